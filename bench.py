@@ -1,0 +1,405 @@
+#!/usr/bin/env python
+"""Benchmark of the SHIRO distributed SpMM hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P bench.py --gpus N ...
+
+A step = one shiro_spmm (all of DESIGN.md rows E1-E6) over the config's
+synthetic matrix, 1D row-partitioned over the N ranks (P = N), with B and C
+resident in HBM.  The plan (rows P1-P4) is built once before timing (PAPER.md
+L300: "performed offline ... reused across multiple SpMM operations").
+L2 is flushed (a 256 MiB device memset) before every timed step; each step is
+bracketed by synchronize + barrier and timed with CUDA events on the
+launching stream; the per-step time is the max over ranks.
+
+Prints ONE JSON line on rank 0 (see DESIGN.md section 6 for every field).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "SpMM GFLOP/s (2·nnz·N) at 1/2/4/8 B200 + bytes communicated vs oblivious"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+NVLINK_GBS = 770.0   # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return dict(PEAKS_FALLBACK)
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms."""
+    Q = ("index,clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = str(gpu_index)
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms",
+                 "100", "-i", self.gpu], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 8]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        busy = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit() and
+                r[3].isdigit() and int(r[3]) > 0]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(busy or sm) if sm else None,
+                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows), "samples_busy": len(busy)}
+
+
+# ----------------------------------------------------------------- roofline
+def op_bytes(info, N, op):
+    """Algorithmic (compulsory) HBM bytes of one launch of device op `op`
+    (DESIGN.md section 5): CSR index+value 8 B per nonzero, row_ptr 8 B per
+    row, out_row 4 B per row, every distinct source row read once (4N B),
+    every output row written once (4N B), accumulating ops also read it."""
+    z, r, s = info["op_nnz"][op], info["op_rows"][op], info["op_src_rows"][op]
+    row = 4 * N
+    if op == "pack":
+        return 8 * r + row * s + row * r
+    if op == "scatter":
+        return 12 * r + 4 * z + row * s + 2 * row * r
+    b = 8 * z + 8 * (r + 1) + row * s + row * r
+    if op != "local":
+        b += 4 * r                       # out_row map
+    if op == "remote":
+        b += row * r                     # C read-modify-write
+    return b
+
+
+STAGE_OF_OP = {"local": "local", "partial": "partial", "remote": "remote",
+               "scatter": "scatter", "pack": "pack"}
+
+
+def traffic_from_profiles(config, world, op):
+    """dram bytes per launch from a committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    return d.get(f"{config}/P{world}/{op}")
+
+
+# ----------------------------------------------------------------- reference arm
+def run_reference(args, cfg, world, rank):
+    """The oracle (as it stands) on the host cores: each step computes the
+    fp64 product of a bounded row sample of the same matrix."""
+    if rank != 0:
+        return
+    import oracle
+    import shiro_gen
+    row_ptr, col, val = shiro_gen.gen_matrix(cfg, cache_dir=_cache_dir())
+    B = shiro_gen.gen_B(cfg.seed, 0, cfg.n, cfg.N)
+    rows, nnz_s = _sample_rows(row_ptr, budget_nnz=1_500_000)
+    cores = os.cpu_count()
+    for _ in range(args.warmup):
+        oracle.spmm_ref(row_ptr, col, val, B, rows=rows)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.spmm_ref(row_ptr, col, val, B, rows=rows)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.mean(ts)
+    v = 2 * nnz_s * cfg.N / t / 1e9
+    sample = f"{rows.size} of {cfg.n} rows ({nnz_s} of {int(row_ptr[-1])} nnz), fp64 oracle"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "GFLOP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.desc}", "n": cfg.n, "nnz": cfg.nnz,
+                   "N": cfg.N, "P": world},
+        "cpu_baseline": {"value": round(v, 3), "unit": "GFLOP/s", "cores": cores,
+                         "kind": "oracle", "sample": sample},
+        "e2e": {"value": round(v, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def _sample_rows(row_ptr, budget_nnz):
+    """Evenly strided rows whose nonzeros total about budget_nnz (all rows if
+    the matrix is smaller)."""
+    n = row_ptr.size - 1
+    nnz = int(row_ptr[-1])
+    if nnz <= budget_nnz:
+        rows = np.arange(n, dtype=np.int64)
+    else:
+        stride = max(1, int(np.ceil(nnz / budget_nnz)))
+        rows = np.arange(0, n, stride, dtype=np.int64)
+    deg = row_ptr[rows + 1] - row_ptr[rows]
+    return rows, int(deg.sum())
+
+
+def _cache_dir():
+    return os.environ.get("SHIRO_GEN_CACHE", "/tmp/shiro_gen_cache")
+
+
+def cpu_baseline(cfg, row_ptr, col, val, B_full, target_s=10.0):
+    """The oracle's fp64 product on the host cores (rank 0, N=1 only): the
+    full matrix repeated (or a row sample) for about target_s seconds."""
+    import oracle
+    rows, nnz_s = _sample_rows(row_ptr, budget_nnz=20_000_000)
+    t0 = time.perf_counter()
+    oracle.spmm_ref(row_ptr, col, val, B_full, rows=rows)
+    t1 = time.perf_counter() - t0
+    reps = max(1, int(target_s / max(t1, 1e-3)))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        oracle.spmm_ref(row_ptr, col, val, B_full, rows=rows)
+    t = (time.perf_counter() - t0) / reps
+    return {"value": round(2 * nnz_s * cfg.N / t / 1e9, 3), "unit": "GFLOP/s",
+            "cores": os.cpu_count(), "kind": "oracle",
+            "sample": f"{rows.size} of {cfg.n} rows ({nnz_s} nnz) x {reps} repetitions, "
+                      f"fp64 accumulation, OpenMP over rows, {t * reps:.1f} s total"}
+
+
+# ----------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--group-size", type=int, default=1)
+    ap.add_argument("--fused", action="store_true", help="SHIRO_F_FUSED_RECV")
+    ap.add_argument("--colmax", action="store_true", help="SHIRO_F_COVER_COLMAX")
+    ap.add_argument("--mode", default="joint", choices=["joint", "col", "row"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    import shiro_gen
+    cfg = shiro_gen.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg, world, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2512_20178_b200 as sh
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    row_ptr, col, val = shiro_gen.gen_matrix(cfg, cache_dir=_cache_dir())
+    nnz = int(row_ptr[-1])
+    part = sh.uniform_partition(cfg.n, world)
+    lo, hi = int(part[rank]), int(part[rank + 1])
+    M = hi - lo
+    rp_l, col_l, val_l = sh.local_rows(row_ptr, col, val, part, rank)
+    B_p = shiro_gen.gen_B(cfg.seed, lo, M, cfg.N)
+
+    flags = 0
+    if args.fused:
+        flags |= sh.F_FUSED_RECV
+    if args.colmax:
+        flags |= sh.F_COVER_COLMAX
+    flags |= {"joint": 0, "col": sh.F_MODE_COL, "row": sh.F_MODE_ROW}[args.mode]
+    nccl_id = None
+    if world > 1:
+        obj = [sh.get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    plan = sh.Plan.distributed(rank, world, cfg.n, part, rp_l, col_l, val_l, cfg.N,
+                               group_size=args.group_size, flags=flags, nccl_id=nccl_id)
+    info = plan.info()
+
+    Bd = torch.from_numpy(B_p).to(dev)
+    Cd = torch.empty((M, cfg.N), device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    for _ in range(args.warmup):
+        plan.spmm(Bd, Cd, stream)
+    torch.cuda.synchronize()
+    barrier()
+
+    plan.profile(True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    step_ms, stages = [], []
+    launches = 0
+    for k in range(args.steps):
+        flush.zero_()                                   # L2 flush, outside the timed window
+        torch.cuda.synchronize()
+        barrier()
+        ev[k][0].record(stream)
+        plan.spmm(Bd, Cd, stream)
+        ev[k][1].record(stream)
+        torch.cuda.synchronize()
+        step_ms.append(ev[k][0].elapsed_time(ev[k][1]))
+        stages.append(plan.stage_times())
+        launches += plan.last_launches()
+    barrier()
+    clk = clocks.stop()
+    plan.profile(False)
+
+    # max over ranks, per step and per stage
+    t = torch.tensor(step_ms, dtype=torch.float64, device=dev)
+    st = torch.tensor([[s[x] for x in sh.STAGES] for s in stages], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(st, op=dist.ReduceOp.MAX)
+    step_ms = t.cpu().numpy()
+    stage_ms = dict(zip(sh.STAGES, st.mean(0).cpu().numpy().tolist()))
+    ms = float(step_ms.mean())
+    value = 2.0 * nnz * cfg.N / (ms * 1e-3) / 1e9
+
+    # roofline of the dominant kernel (largest mean stage among kernels)
+    peaks = load_peaks()
+    kern = {op: stage_ms[STAGE_OF_OP[op]] for op in sh.OPS if info["op_rows"][op] > 0}
+    dom = max(kern, key=kern.get) if kern else "local"
+    dom_ms = max(kern.get(dom, 0.0), 1e-9)
+    ab = op_bytes(info, cfg.N, dom)
+    ab_all = torch.tensor([float(ab)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ab_all, op=dist.ReduceOp.MAX)
+    achieved = float(ab_all.item()) / (dom_ms * 1e-3) / 1e9
+    roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
+            "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
+            "traffic": traffic_from_profiles(args.config, world, dom),
+            "algorithmic_bytes": int(ab_all.item()), "launch_ms": round(dom_ms, 5),
+            "peak_source": peaks["source"],
+            "gather_bytes": int(4 * cfg.N * info["op_nnz"][dom]) if dom != "pack" else None}
+
+    # exchange (NVLink) achieved bandwidth, per rank max(send, recv) bytes
+    xbytes = 4 * cfg.N * max(info["send_b_rows"] + info["send_c_rows"],
+                             info["recv_b_rows"] + info["recv_c_rows"])
+    xb = torch.tensor([float(xbytes)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(xb, op=dist.ReduceOp.MAX)
+    exch = None
+    if world > 1 and stage_ms["exchange"] > 0:
+        gbs = xb.item() / (stage_ms["exchange"] * 1e-3) / 1e9
+        exch = {"bytes_max_rank": int(xb.item()), "ms": round(stage_ms["exchange"], 5),
+                "achieved_gbs": round(gbs, 1), "peak_gbs": NVLINK_GBS,
+                "frac": round(gbs / NVLINK_GBS, 4)}
+
+    # end to end through the public API with host buffers (pinned)
+    e2e = None
+    if not args.no_e2e:
+        Bh = torch.from_numpy(B_p).pin_memory()
+        Ch = torch.empty((M, cfg.N)).pin_memory()
+        plan.spmm_host(Bh, Ch, stream)
+        tt = []
+        for _ in range(args.steps):
+            torch.cuda.synchronize()
+            barrier()
+            t0 = time.perf_counter()
+            plan.spmm_host(Bh, Ch, stream)
+            tt.append(time.perf_counter() - t0)
+        te = torch.tensor(tt, dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        te_mean = float(te.mean().item())
+        e2e = {"value": round(2.0 * nnz * cfg.N / te_mean / 1e9, 3), "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int(B_p.nbytes) * world,
+               "d2h_bytes_per_step": int(M * cfg.N * 4) * world,
+               "ms_per_step": round(te_mean * 1e3, 4)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        B_full = B_p if world == 1 else shiro_gen.gen_B(cfg.seed, 0, cfg.n, cfg.N)
+        cpu = cpu_baseline(cfg, row_ptr, col, val, B_full)
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 5),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: {cfg.desc}", "n": cfg.n, "nnz": nnz, "N": cfg.N,
+                       "P": world, "group_size": args.group_size,
+                       "plan": ("fused-recv " if args.fused else "") + args.mode +
+                               (" col-max" if args.colmax else " row-max"),
+                       "partition": "uniform 1D rows (larger blocks first)",
+                       "l2": "flushed (256 MiB memset) before every timed step",
+                       "parallelism": f"1D row partition over {world} rank(s), NCCL all-to-allv"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "bytes": {"joint": info["g_joint_rows"] * 4 * cfg.N,
+                      "oblivious_allgather": info["g_oblivious_rows"] * 4 * cfg.N,
+                      "col_based": info["g_col_rows"] * 4 * cfg.N,
+                      "row_based": info["g_row_rows"] * 4 * cfg.N,
+                      "block": info["g_block_rows"] * 4 * cfg.N,
+                      "joint_vs_oblivious": (info["g_joint_rows"] / info["g_oblivious_rows"])
+                      if info["g_oblivious_rows"] else None,
+                      "setup_bytes": info["g_setup_bytes"]},
+            "exchange": exch,
+            "stages_ms": {k: round(v, 5) for k, v in stage_ms.items()},
+            "step_ms": {"median": round(float(np.median(step_ms)), 5),
+                        "p10": round(float(np.percentile(step_ms, 10)), 5),
+                        "p90": round(float(np.percentile(step_ms, 90)), 5)},
+            "plan_seconds": round(info["plan_seconds"], 3),
+        }
+        print(json.dumps(out), flush=True)
+    plan.free()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,408 @@
+// kernels.cu -- hand-written sm_100a kernels of the SHIRO hot path.
+//
+// The dense width N of B and C is the contraction-free axis of SpMM: every
+// nonzero a_ij contributes a length-N axpy of row j of the source into row i
+// of the output.  The work is a memory-bound gather, so
+// the kernels are designed around HBM3e / L2 traffic, not tensor cores:
+//   * a row of the source is N*4 bytes (512 B at N = 128); a group of
+//     LPR = min(32, N/4) lanes owns one output row and moves it with 128-bit
+//     loads (float4) -- one fully coalesced LDG.128 per lane per nonzero;
+//   * the row's (col, val) pairs are loaded cooperatively (one pair per lane,
+//     streamed with L1::no_allocate) and broadcast with shuffles, then U = 8
+//     independent row gathers are issued before any FMA (memory-level
+//     parallelism for short power-law rows);
+//   * accumulation is fp32 in registers, one store per output row;
+//   * rows longer than L nonzeros (hubs) are split into chunk tasks that run
+//     first; their partials are reduced in chunk order by the last-arriving
+//     chunk (threadfence + arrival counter): deterministic, single launch.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kernels.h"
+
+namespace shiro {
+
+namespace {
+
+constexpr int kBlock = 256;   // 8 warps per CTA
+constexpr int kUnroll = 8;    // outstanding row gathers per lane group
+
+__device__ __forceinline__ int ld_stream_i32(const int32_t *p) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float ld_stream_f32(const float *p) {
+  float v;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int64_t ld_i64(const int64_t *p) { return __ldg(p); }
+
+__device__ __forceinline__ void fma4(float4 &acc, float v, const float4 &x) {
+  acc.x = fmaf(v, x.x, acc.x);
+  acc.y = fmaf(v, x.y, acc.y);
+  acc.z = fmaf(v, x.z, acc.z);
+  acc.w = fmaf(v, x.w, acc.w);
+}
+__device__ __forceinline__ void add4(float4 &acc, const float4 &x) {
+  acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+}
+
+// Source row pointer in the unified row space [X0 || X1].
+__device__ __forceinline__ const float4 *src_row(const SpmmArgs &a, int c) {
+  const float *base = (c < a.n0) ? a.X0 + (int64_t)c * a.N : a.X1 + (int64_t)(c - a.n0) * a.N;
+  return reinterpret_cast<const float4 *>(base);
+}
+
+// acc[v] += sum_{k in [kb, ke)} val[k] * X(col[k])[(li + v*LPR)*4 .. +3]
+template <int LPR, int VPL>
+__device__ __forceinline__ void accum_range(float4 (&acc)[VPL], const SpmmArgs &a, int64_t kb,
+                                            int64_t ke, int li, unsigned mask) {
+  constexpr int U = (LPR < kUnroll) ? LPR : kUnroll;
+  for (int64_t base = kb; base < ke; base += LPR) {
+    const int64_t k = base + li;
+    int c = 0;
+    float v = 0.f;
+    if (k < ke) {
+      c = ld_stream_i32(a.col + k);
+      v = a.val ? ld_stream_f32(a.val + k) : 1.f;
+    }
+    const int cnt = (int)((ke - base) < LPR ? (ke - base) : LPR);
+    for (int j = 0; j < cnt; j += U) {
+      float4 x[U][VPL];
+      float w[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int cu = __shfl_sync(mask, c, j + u, LPR);
+        const float vu = __shfl_sync(mask, v, j + u, LPR);
+        if (j + u < cnt) {            // uniform across the lane group
+          const float4 *r = src_row(a, cu);
+#pragma unroll
+          for (int q = 0; q < VPL; ++q) x[u][q] = __ldg(r + li + q * LPR);
+          w[u] = vu;
+        } else {
+#pragma unroll
+          for (int q = 0; q < VPL; ++q) x[u][q] = make_float4(0.f, 0.f, 0.f, 0.f);
+          w[u] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) fma4(acc[q], w[u], x[u][q]);
+    }
+  }
+}
+
+template <int LPR, int VPL, bool ACCUM>
+__global__ void __launch_bounds__(kBlock) k_spmm(const SpmmArgs a) {
+  constexpr int R = 32 / LPR;   // output rows per warp
+  const int lane = threadIdx.x & 31;
+  const int sub = lane / LPR;
+  const int li = lane % LPR;
+  const unsigned mask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (sub * LPR));
+  const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const int64_t u = warp * R + sub;     // work unit: chunk task, then regular row
+
+  float4 acc[VPL];
+#pragma unroll
+  for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+
+  if (u < a.n_tasks) {
+    // ---- chunk of a long (hub) row -------------------------------------
+    const int lr = a.task_long[u];
+    const int64_t t = a.long_row[lr];
+    const int f = a.long_first[lr], nch = a.long_first[lr + 1] - f;
+    const int64_t rb = ld_i64(a.rp + t), re = ld_i64(a.rp + t + 1);
+    const int64_t kb = rb + (int64_t)(u - f) * a.L;
+    const int64_t ke = (kb + a.L < re) ? kb + a.L : re;
+    accum_range<LPR, VPL>(acc, a, kb, ke, li, mask);
+    float4 *sp = reinterpret_cast<float4 *>(a.scratch + u * (int64_t)a.N);
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) __stcg(sp + li + q * LPR, acc[q]);
+    __threadfence();
+    __syncwarp(mask);
+    int last = 0;
+    if (li == 0) last = (atomicAdd(a.long_counter + lr, 1) == nch - 1);
+    last = __shfl_sync(mask, last, 0, LPR);
+    if (last) {
+      __threadfence();
+      float4 s[VPL];
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) s[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int c = 0; c < nch; ++c) {        // fixed chunk order: deterministic
+        const float4 *cp = reinterpret_cast<const float4 *>(a.scratch + (int64_t)(f + c) * a.N);
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) add4(s[q], __ldcg(cp + li + q * LPR));
+      }
+      const int64_t orow = a.out_row ? a.out_row[t] : t;
+      float4 *y = reinterpret_cast<float4 *>(a.Y + orow * a.N);
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) {
+        if (ACCUM) {
+          float4 o = y[li + q * LPR];
+          add4(o, s[q]);
+          s[q] = o;
+        }
+        y[li + q * LPR] = s[q];
+      }
+      if (li == 0) a.long_counter[lr] = 0;    // re-arm for the next launch
+    }
+    return;
+  }
+  const int64_t t = u - a.n_tasks;
+  if (t >= a.nrows) return;
+  const int64_t kb = ld_i64(a.rp + t), ke = ld_i64(a.rp + t + 1);
+  if (ke - kb > a.L) return;              // handled by chunk tasks
+  accum_range<LPR, VPL>(acc, a, kb, ke, li, mask);
+  const int64_t orow = a.out_row ? a.out_row[t] : t;
+  float4 *y = reinterpret_cast<float4 *>(a.Y + orow * a.N);
+#pragma unroll
+  for (int q = 0; q < VPL; ++q) {
+    if (ACCUM) add4(acc[q], y[li + q * LPR]);
+    y[li + q * LPR] = acc[q];
+  }
+}
+
+// Generic width (N % 4 != 0 or N not a supported vector width): one warp per
+// row, lanes stride over columns; no row splitting.  Correctness path.
+template <bool ACCUM>
+__global__ void __launch_bounds__(kBlock) k_spmm_generic(const SpmmArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  if (t >= a.nrows) return;
+  const int64_t kb = a.rp[t], ke = a.rp[t + 1];
+  const int64_t orow = a.out_row ? a.out_row[t] : t;
+  float *y = a.Y + orow * a.N;
+  for (int c0 = 0; c0 < a.N; c0 += 32 * 4) {
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int64_t k = kb; k < ke; ++k) {
+      const int c = a.col[k];
+      const float v = a.val ? a.val[k] : 1.f;
+      const float *r = (c < a.n0) ? a.X0 + (int64_t)c * a.N : a.X1 + (int64_t)(c - a.n0) * a.N;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int x = c0 + lane + 32 * q;
+        if (x < a.N) acc[q] = fmaf(v, __ldg(r + x), acc[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int x = c0 + lane + 32 * q;
+      if (x < a.N) y[x] = ACCUM ? y[x] + acc[q] : acc[q];
+    }
+  }
+}
+
+template <int LPR, int VPL>
+__global__ void __launch_bounds__(kBlock) k_pack(int64_t n, const int32_t *__restrict__ src,
+                                                 const int32_t *__restrict__ dst,
+                                                 const float *__restrict__ X, float *__restrict__ Y,
+                                                 int N) {
+  constexpr int R = 32 / LPR;
+  constexpr int RPU = 4;   // rows per lane group: 4 loads in flight before the stores
+  const int lane = threadIdx.x & 31;
+  const int sub = lane / LPR, li = lane % LPR;
+  const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const int64_t u0 = (warp * R + sub) * RPU;
+  float4 x[RPU][VPL];
+#pragma unroll
+  for (int r = 0; r < RPU; ++r) {
+    if (u0 + r < n) {
+      const float4 *s = reinterpret_cast<const float4 *>(X + (int64_t)__ldg(src + u0 + r) * N);
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) x[r][q] = __ldg(s + li + q * LPR);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RPU; ++r) {
+    if (u0 + r < n) {
+      float4 *d = reinterpret_cast<float4 *>(Y + (int64_t)__ldg(dst + u0 + r) * N);
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) d[li + q * LPR] = x[r][q];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k_pack_generic(int64_t n, const int32_t *src,
+                                                         const int32_t *dst, const float *X,
+                                                         float *Y, int N) {
+  const int lane = threadIdx.x & 31;
+  const int64_t u = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  if (u >= n) return;
+  const float *s = X + (int64_t)src[u] * N;
+  float *d = Y + (int64_t)dst[u] * N;
+  for (int x = lane; x < N; x += 32) d[x] = s[x];
+}
+
+template <int LPR, int VPL>
+__global__ void __launch_bounds__(kBlock) k_scatter_add(int64_t nt, const int32_t *__restrict__ tgt,
+                                                        const int64_t *__restrict__ ptr,
+                                                        const int32_t *__restrict__ srcrow,
+                                                        const float *__restrict__ Rb,
+                                                        float *__restrict__ C, int N) {
+  constexpr int R = 32 / LPR;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane / LPR, li = lane % LPR;
+  const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const int64_t u = warp * R + sub;
+  if (u >= nt) return;
+  const int64_t kb = __ldg(ptr + u), ke = __ldg(ptr + u + 1);
+  float4 *c = reinterpret_cast<float4 *>(C + (int64_t)__ldg(tgt + u) * N);
+  float4 acc[VPL];
+#pragma unroll
+  for (int q = 0; q < VPL; ++q) acc[q] = c[li + q * LPR];
+  // at most P-1 partials per row (plus hierarchical aggregates): load all
+  // partial rows of a chunk of 4 before adding, in source order
+  for (int64_t k = kb; k < ke; k += 4) {
+    float4 x[4][VPL];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      if (k + r < ke) {
+        const float4 *s = reinterpret_cast<const float4 *>(Rb + (int64_t)__ldg(srcrow + k + r) * N);
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) x[r][q] = __ldcs(s + li + q * LPR);
+      } else {
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) x[r][q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) add4(acc[q], x[r][q]);
+  }
+#pragma unroll
+  for (int q = 0; q < VPL; ++q) c[li + q * LPR] = acc[q];
+}
+
+__global__ void __launch_bounds__(kBlock) k_scatter_add_generic(int64_t nt, const int32_t *tgt,
+                                                                const int64_t *ptr,
+                                                                const int32_t *srcrow,
+                                                                const float *Rb, float *C, int N) {
+  const int lane = threadIdx.x & 31;
+  const int64_t u = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  if (u >= nt) return;
+  float *c = C + (int64_t)tgt[u] * N;
+  for (int x = lane; x < N; x += 32) {
+    float acc = c[x];
+    for (int64_t k = ptr[u]; k < ptr[u + 1]; ++k) acc += Rb[(int64_t)srcrow[k] * N + x];
+    c[x] = acc;
+  }
+}
+
+// Vector shape for width N: LPR lanes per row, VPL float4 per lane.
+bool vec_shape(int N, int *lpr, int *vpl) {
+  switch (N) {
+    case 4: *lpr = 1; *vpl = 1; return true;
+    case 8: *lpr = 2; *vpl = 1; return true;
+    case 16: *lpr = 4; *vpl = 1; return true;
+    case 32: *lpr = 8; *vpl = 1; return true;
+    case 64: *lpr = 16; *vpl = 1; return true;
+    case 128: *lpr = 32; *vpl = 1; return true;
+    case 256: *lpr = 32; *vpl = 2; return true;
+    case 512: *lpr = 32; *vpl = 4; return true;
+    default: return false;
+  }
+}
+
+inline int64_t blocks_for(int64_t units, int rows_per_warp) {
+  const int64_t per_block = (int64_t)(kBlock / 32) * rows_per_warp;
+  return (units + per_block - 1) / per_block;
+}
+
+template <int LPR, int VPL>
+void spmm_shape(const SpmmArgs &a, bool acc, cudaStream_t s) {
+  const int64_t units = a.n_tasks + a.nrows;
+  const int64_t grid = blocks_for(units, 32 / LPR);
+  if (acc)
+    k_spmm<LPR, VPL, true><<<(unsigned)grid, kBlock, 0, s>>>(a);
+  else
+    k_spmm<LPR, VPL, false><<<(unsigned)grid, kBlock, 0, s>>>(a);
+}
+
+template <int LPR, int VPL>
+void pack_shape(int64_t n, const int32_t *src, const int32_t *dst, const float *X, float *Y,
+                int N, cudaStream_t s) {
+  const int64_t grid = blocks_for((n + 3) / 4, 32 / LPR);
+  k_pack<LPR, VPL><<<(unsigned)grid, kBlock, 0, s>>>(n, src, dst, X, Y, N);
+}
+
+template <int LPR, int VPL>
+void scatter_shape(int64_t nt, const int32_t *tgt, const int64_t *ptr, const int32_t *src,
+                   const float *R, float *C, int N, cudaStream_t s) {
+  const int64_t grid = blocks_for(nt, 32 / LPR);
+  k_scatter_add<LPR, VPL><<<(unsigned)grid, kBlock, 0, s>>>(nt, tgt, ptr, src, R, C, N);
+}
+
+#define SHIRO_DISPATCH(N, FN, ...)                        \
+  do {                                                    \
+    int lpr_, vpl_;                                       \
+    vec_shape(N, &lpr_, &vpl_);                           \
+    if (lpr_ == 1) FN<1, 1>(__VA_ARGS__);                 \
+    else if (lpr_ == 2) FN<2, 1>(__VA_ARGS__);            \
+    else if (lpr_ == 4) FN<4, 1>(__VA_ARGS__);            \
+    else if (lpr_ == 8) FN<8, 1>(__VA_ARGS__);            \
+    else if (lpr_ == 16) FN<16, 1>(__VA_ARGS__);          \
+    else if (vpl_ == 1) FN<32, 1>(__VA_ARGS__);           \
+    else if (vpl_ == 2) FN<32, 2>(__VA_ARGS__);           \
+    else FN<32, 4>(__VA_ARGS__);                          \
+  } while (0)
+
+}  // namespace
+
+bool vec_shape_public(int N, int *lpr, int *vpl) { return vec_shape(N, lpr, vpl); }
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (!n) n = 148;
+  }
+  return n;
+}
+
+int launch_spmm(const SpmmArgs &a, bool accumulate, cudaStream_t s) {
+  if (a.nrows == 0 && a.n_tasks == 0) return 0;
+  int lpr, vpl;
+  if (vec_shape(a.N, &lpr, &vpl)) {
+    SHIRO_DISPATCH(a.N, spmm_shape, a, accumulate, s);
+  } else {
+    const int64_t grid = blocks_for(a.nrows, 1);
+    if (accumulate)
+      k_spmm_generic<true><<<(unsigned)grid, kBlock, 0, s>>>(a);
+    else
+      k_spmm_generic<false><<<(unsigned)grid, kBlock, 0, s>>>(a);
+  }
+  return 1;
+}
+
+int launch_pack(int64_t n, const int32_t *src, const int32_t *dst, const float *X, float *Y,
+                int32_t N, cudaStream_t s) {
+  if (n == 0) return 0;
+  int lpr, vpl;
+  if (vec_shape(N, &lpr, &vpl)) {
+    SHIRO_DISPATCH(N, pack_shape, n, src, dst, X, Y, N, s);
+  } else {
+    k_pack_generic<<<(unsigned)blocks_for(n, 1), kBlock, 0, s>>>(n, src, dst, X, Y, N);
+  }
+  return 1;
+}
+
+int launch_scatter_add(int64_t nt, const int32_t *tgt, const int64_t *ptr, const int32_t *src,
+                       const float *R, float *C, int32_t N, cudaStream_t s) {
+  if (nt == 0) return 0;
+  int lpr, vpl;
+  if (vec_shape(N, &lpr, &vpl)) {
+    SHIRO_DISPATCH(N, scatter_shape, nt, tgt, ptr, src, R, C, N, s);
+  } else {
+    k_scatter_add_generic<<<(unsigned)blocks_for(nt, 1), kBlock, 0, s>>>(nt, tgt, ptr, src, R, C,
+                                                                          N);
+  }
+  return 1;
+}
+
+}  // namespace shiro

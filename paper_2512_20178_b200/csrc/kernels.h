@@ -1,0 +1,52 @@
+// kernels.h -- internal launch interface of the sm_100a kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace shiro {
+
+// One CSR SpMM launch (K1/K2/K3 of DESIGN.md):
+//   Y[out_row[t]] (+)= sum_{k in [rp[t], rp[t+1])} val[k] * X(col[k])
+// with X(c) = X0[c] for c < n0 and X1[c - n0] otherwise (unified source row
+// space, e.g. [B_local || receive buffer]).  val == nullptr means all ones.
+// out_row == nullptr means out_row[t] = t.  Rows with more than L nonzeros
+// are split into chunk tasks of L nonzeros (power-law hub rows); the chunk
+// partials are reduced in a fixed order by the last-arriving chunk, so the
+// result is deterministic.
+struct SpmmArgs {
+  int64_t nrows = 0;
+  const int64_t *rp = nullptr;
+  const int32_t *col = nullptr;
+  const float *val = nullptr;
+  const int32_t *out_row = nullptr;
+  const float *X0 = nullptr;
+  int64_t n0 = 0;
+  const float *X1 = nullptr;
+  float *Y = nullptr;
+  int32_t N = 0;
+  int32_t L = 0x7fffffff;         // split threshold
+  int32_t n_tasks = 0;            // chunk tasks (long rows)
+  const int32_t *task_long = nullptr;   // [n_tasks] long-row index of each task
+  const int32_t *long_row = nullptr;    // [n_long] CSR row t of each long row
+  const int32_t *long_first = nullptr;  // [n_long+1] first task of each long row
+  int32_t *long_counter = nullptr;      // [n_long] zero-initialised arrival counters
+  float *scratch = nullptr;             // [n_tasks * N] chunk partials
+};
+
+// accumulate: false -> Y = A*X (overwrite, empty rows get zeros); true -> Y += A*X
+// returns the number of kernel launches issued (0 if nothing to do)
+int launch_spmm(const SpmmArgs &a, bool accumulate, cudaStream_t s);
+
+// K4: Y[dst[i]] = X[src[i]] for i < n (gather B rows into the send buffer)
+int launch_pack(int64_t n, const int32_t *src, const int32_t *dst, const float *X, float *Y,
+                int32_t N, cudaStream_t s);
+
+// K5: C[tgt[u]] += sum_{k in [ptr[u], ptr[u+1])} R[src[k]] (gather-sum of
+// received partial C rows, fixed order: C first, then sources ascending)
+int launch_scatter_add(int64_t nt, const int32_t *tgt, const int64_t *ptr, const int32_t *src,
+                       const float *R, float *C, int32_t N, cudaStream_t s);
+
+// SM count of the current device (cached)
+int num_sms();
+
+}  // namespace shiro

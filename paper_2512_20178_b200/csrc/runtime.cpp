@@ -1,0 +1,799 @@
+// runtime.cpp -- device upload, executor, transports and the C ABI.
+//
+// Per-iteration flow of the flat joint plan (workflow
+// steps 3-5; DESIGN.md rows E1-E6), on the caller's stream s0 and an internal
+// communication stream s1:
+//   s0: K4 pack B rows -> send_buf      (E1, "prepares required B rows")
+//   s0: K3 A_out * B   -> send_buf      (E2, "computes partial C results")
+//   s0: record ev_packed
+//   s1: wait ev_packed; NCCL grouped send/recv per peer (E3, all-to-allv)
+//   s0: K1 C = A_diag * B               (E4, overlapped with E3)
+//   s0: wait ev_recvd
+//   s0: K2 C += A_col * recv_B          (E5)
+//   s0: K5 C += sum of recv partials     (E6)   [or K2+K5 fused: FUSED_RECV]
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <mutex>
+
+#include "shiro_internal.h"
+
+namespace shiro {
+
+Plan::~Plan() {
+  if (!loopback_view) {
+    if (comm) ncclCommDestroy(comm);
+    if (ev_packed) cudaEventDestroy(ev_packed);
+    if (ev_recvd) cudaEventDestroy(ev_recvd);
+    if (comm_stream) cudaStreamDestroy(comm_stream);
+    if (arena) cudaFree(arena);
+    if (stage) cudaFree(stage);
+    for (auto &e : prof)
+      if (e) cudaEventDestroy(e);
+  }
+}
+
+namespace {
+
+// ---------------------------------------------------------------- arena
+struct Arena {
+  struct Item { size_t off; const void *src; size_t bytes; };
+  std::vector<Item> items;
+  size_t total = 0;
+  size_t reserve(size_t bytes, const void *src = nullptr) {
+    size_t off = (total + 255) & ~size_t(255);
+    total = off + bytes;
+    items.push_back({off, src, bytes});
+    return off;
+  }
+};
+
+template <typename T>
+size_t put(Arena &ar, const std::vector<T> &v) {
+  return ar.reserve(v.size() * sizeof(T), v.empty() ? nullptr : v.data());
+}
+
+// Row-split threshold L for one op: hub rows are cut into chunks of L
+// nonzeros so that no single lane group holds the tail (power-law inputs).
+int32_t split_threshold(int64_t nnz) {
+  int64_t L = nnz / ((int64_t)num_sms() * 64);
+  L = std::max<int64_t>(128, std::min<int64_t>(4096, L));
+  return (int32_t)L;
+}
+
+struct SplitHost {
+  int32_t L = 0x7fffffff;
+  std::vector<int32_t> task_long, long_row, long_first{0};
+};
+
+SplitHost make_split(const HostCsr &c, int N) {
+  SplitHost s;
+  int lpr, vpl;
+  if (!vec_shape_public(N, &lpr, &vpl)) return s;   // generic path: no split
+  s.L = split_threshold(c.nnz());
+  for (int64_t t = 0; t < c.nrows; ++t) {
+    const int64_t d = c.rp[t + 1] - c.rp[t];
+    if (d > s.L) {
+      const int32_t lr = (int32_t)s.long_row.size();
+      s.long_row.push_back((int32_t)t);
+      const int64_t nch = (d + s.L - 1) / s.L;
+      for (int64_t k = 0; k < nch; ++k) s.task_long.push_back(lr);
+      s.long_first.push_back((int32_t)s.task_long.size());
+    }
+  }
+  return s;
+}
+
+struct SpmmLayout {
+  size_t rp, col, val, out, tl, lrow, lfirst, cnt, scratch;
+  SplitHost sp;
+  bool has_val, has_out;
+};
+
+SpmmLayout layout_spmm(Arena &ar, const HostCsr &c, int N) {
+  SpmmLayout L;
+  L.sp = make_split(c, N);
+  L.rp = put(ar, c.rp);
+  L.col = put(ar, c.col);
+  L.has_val = !c.val.empty();
+  L.has_out = !c.out_row.empty();
+  L.val = put(ar, c.val);
+  L.out = put(ar, c.out_row);
+  L.tl = put(ar, L.sp.task_long);
+  L.lrow = put(ar, L.sp.long_row);
+  L.lfirst = put(ar, L.sp.long_first);
+  L.cnt = ar.reserve(L.sp.long_row.size() * sizeof(int32_t));          // zeroed
+  L.scratch = ar.reserve(L.sp.task_long.size() * (size_t)N * sizeof(float));
+  return L;
+}
+
+DevSpmm bind_spmm(char *base, const SpmmLayout &L, const HostCsr &c, int N) {
+  DevSpmm d;
+  SpmmArgs &a = d.a;
+  a.nrows = c.nrows;
+  a.rp = reinterpret_cast<const int64_t *>(base + L.rp);
+  a.col = reinterpret_cast<const int32_t *>(base + L.col);
+  a.val = L.has_val ? reinterpret_cast<const float *>(base + L.val) : nullptr;
+  a.out_row = L.has_out ? reinterpret_cast<const int32_t *>(base + L.out) : nullptr;
+  a.N = N;
+  a.L = L.sp.L;
+  a.n_tasks = (int32_t)L.sp.task_long.size();
+  a.task_long = reinterpret_cast<const int32_t *>(base + L.tl);
+  a.long_row = reinterpret_cast<const int32_t *>(base + L.lrow);
+  a.long_first = reinterpret_cast<const int32_t *>(base + L.lfirst);
+  a.long_counter = reinterpret_cast<int32_t *>(base + L.cnt);
+  a.scratch = reinterpret_cast<float *>(base + L.scratch);
+  d.nnz = c.nnz();
+  return d;
+}
+
+}  // namespace
+
+void plan_upload(Plan &pl, cudaStream_t s) {
+  SHIRO_CK(cudaGetDevice(&pl.device));
+  Arena ar;
+  const int N = pl.N;
+  const size_t o_send = ar.reserve((size_t)pl.send_rows * N * sizeof(float));
+  const size_t o_recv = ar.reserve((size_t)pl.recv_rows * N * sizeof(float));
+  const bool fused = pl.flags & SHIRO_F_FUSED_RECV;
+  SpmmLayout l_diag = layout_spmm(ar, pl.A_diag, N);
+  SpmmLayout l_out = layout_spmm(ar, pl.A_out, N);
+  HostCsr empty;
+  SpmmLayout l_col = layout_spmm(ar, fused ? empty : pl.A_col, N);
+  SpmmLayout l_rem = layout_spmm(ar, fused ? pl.A_rem : empty, N);
+  const size_t o_ps = put(ar, pl.pack_src), o_pd = put(ar, pl.pack_dst);
+  const size_t o_st = put(ar, pl.sc_tgt), o_sp = put(ar, pl.sc_ptr), o_ss = put(ar, pl.sc_src);
+  pl.arena_bytes = std::max<size_t>(ar.total, 256);
+  SHIRO_CK(cudaMalloc(&pl.arena, pl.arena_bytes));
+  SHIRO_CK(cudaMemsetAsync(pl.arena, 0, pl.arena_bytes, s));
+  char *base = static_cast<char *>(pl.arena);
+  for (const auto &it : ar.items)
+    if (it.src && it.bytes)
+      SHIRO_CK(cudaMemcpyAsync(base + it.off, it.src, it.bytes, cudaMemcpyHostToDevice, s));
+  SHIRO_CK(cudaStreamSynchronize(s));
+  pl.send_buf = reinterpret_cast<float *>(base + o_send);
+  pl.recv_buf = reinterpret_cast<float *>(base + o_recv);
+  pl.d_diag = bind_spmm(base, l_diag, pl.A_diag, N);
+  pl.d_out = bind_spmm(base, l_out, pl.A_out, N);
+  pl.d_col = bind_spmm(base, l_col, fused ? empty : pl.A_col, N);
+  pl.d_rem = bind_spmm(base, l_rem, fused ? pl.A_rem : empty, N);
+  pl.d_pack.n = (int64_t)pl.pack_src.size();
+  pl.d_pack.src = reinterpret_cast<const int32_t *>(base + o_ps);
+  pl.d_pack.dst = reinterpret_cast<const int32_t *>(base + o_pd);
+  pl.d_scatter.nt = (int64_t)pl.sc_tgt.size();
+  pl.d_scatter.tgt = reinterpret_cast<const int32_t *>(base + o_st);
+  pl.d_scatter.ptr = reinterpret_cast<const int64_t *>(base + o_sp);
+  pl.d_scatter.src = reinterpret_cast<const int32_t *>(base + o_ss);
+  pl.d_scatter.nsrc = (int64_t)pl.sc_src.size();
+  pl.info.dev_bytes = (int64_t)pl.arena_bytes;
+  // per-op algorithmic work (before the host images are dropped)
+  auto distinct = [](const std::vector<int32_t> &ids) {
+    if (ids.empty()) return (int64_t)0;
+    std::vector<int32_t> v(ids);
+    std::sort(v.begin(), v.end());
+    return (int64_t)(std::unique(v.begin(), v.end()) - v.begin());
+  };
+  auto op = [&](int i, const HostCsr &c) {
+    pl.info.op_nnz[i] = c.nnz();
+    pl.info.op_rows[i] = c.nrows;
+    pl.info.op_src_rows[i] = distinct(c.col);
+  };
+  op(SHIRO_OP_LOCAL, pl.A_diag);
+  op(SHIRO_OP_PARTIAL, pl.A_out);
+  op(SHIRO_OP_REMOTE, fused ? pl.A_rem : pl.A_col);
+  pl.info.op_nnz[SHIRO_OP_SCATTER] = fused ? 0 : (int64_t)pl.sc_src.size();
+  pl.info.op_rows[SHIRO_OP_SCATTER] = fused ? 0 : (int64_t)pl.sc_tgt.size();
+  pl.info.op_src_rows[SHIRO_OP_SCATTER] = fused ? 0 : (int64_t)pl.sc_src.size();
+  pl.info.op_nnz[SHIRO_OP_PACK] = (int64_t)pl.pack_src.size();
+  pl.info.op_rows[SHIRO_OP_PACK] = (int64_t)pl.pack_src.size();
+  pl.info.op_src_rows[SHIRO_OP_PACK] = distinct(pl.pack_src);
+  if (!pl.loopback_view) {
+    SHIRO_CK(cudaStreamCreateWithFlags(&pl.comm_stream, cudaStreamNonBlocking));
+    SHIRO_CK(cudaEventCreateWithFlags(&pl.ev_packed, cudaEventDisableTiming));
+    SHIRO_CK(cudaEventCreateWithFlags(&pl.ev_recvd, cudaEventDisableTiming));
+  }
+  // host images are no longer needed
+  pl.A_diag = HostCsr(); pl.A_out = HostCsr(); pl.A_col = HostCsr(); pl.A_rem = HostCsr();
+  std::vector<int32_t>().swap(pl.pack_src);
+  std::vector<int32_t>().swap(pl.pack_dst);
+  std::vector<int32_t>().swap(pl.sc_tgt);
+  std::vector<int32_t>().swap(pl.sc_src);
+  std::vector<int64_t>(1, 0).swap(pl.sc_ptr);
+}
+
+namespace {
+
+int64_t run_spmm(const DevSpmm &d, const float *X0, int64_t n0, const float *X1, float *Y,
+                 bool accumulate, cudaStream_t s) {
+  if (d.a.nrows == 0) return 0;
+  SpmmArgs a = d.a;
+  a.X0 = X0; a.n0 = n0; a.X1 = X1; a.Y = Y;
+  return launch_spmm(a, accumulate, s);
+}
+
+// E1 + E2: fill the send buffer from B
+int64_t stage_send(Plan &pl, const float *B, cudaStream_t s) {
+  int64_t n = 0;
+  n += launch_pack(pl.d_pack.n, pl.d_pack.src, pl.d_pack.dst, B, pl.send_buf, pl.N, s);
+  n += run_spmm(pl.d_out, B, pl.M, nullptr, pl.send_buf, false, s);
+  return n;
+}
+
+// E5 + E6: consume the receive buffer
+int64_t stage_recv(Plan &pl, float *C, cudaStream_t s) {
+  int64_t n = 0;
+  if (pl.flags & SHIRO_F_FUSED_RECV) {
+    n += run_spmm(pl.d_rem, pl.recv_buf, pl.recv_rows, nullptr, C, true, s);
+  } else {
+    n += run_spmm(pl.d_col, pl.recv_buf, pl.recv_rows, nullptr, C, true, s);
+    n += launch_scatter_add(pl.d_scatter.nt, pl.d_scatter.tgt, pl.d_scatter.ptr, pl.d_scatter.src,
+                            pl.recv_buf, C, pl.N, s);
+  }
+  return n;
+}
+
+int64_t stage_local(Plan &pl, const float *B, float *C, cudaStream_t s) {
+  if (pl.M == 0) return 0;
+  return run_spmm(pl.d_diag, B, pl.M, nullptr, C, false, s);
+}
+
+}  // namespace
+
+void exec_flat(Plan &pl, const float *B, float *C, cudaStream_t s) {
+  // profiling events: 0 start | 1 after pack | 2 after partial | 3,4 exchange
+  // (comm stream) | 5 local start | 6 local end | 7 after remote | 8 end
+  auto rec = [&](int i, cudaStream_t st) {
+    if (pl.prof_on) SHIRO_CK(cudaEventRecord(pl.prof[i], st));
+  };
+  int64_t launches = 0;
+  if (pl.P == 1) {
+    rec(5, s);
+    launches += stage_local(pl, B, C, s);
+    rec(6, s);
+    pl.last_launches = launches;
+    pl.prof_used = 1;
+    return;
+  }
+  const bool overlap = !(pl.flags & SHIRO_F_NO_OVERLAP);
+  rec(0, s);
+  launches += launch_pack(pl.d_pack.n, pl.d_pack.src, pl.d_pack.dst, B, pl.send_buf, pl.N, s);
+  rec(1, s);
+  launches += run_spmm(pl.d_out, B, pl.M, nullptr, pl.send_buf, false, s);
+  rec(2, s);
+  SHIRO_CK(cudaEventRecord(pl.ev_packed, s));
+  SHIRO_CK(cudaStreamWaitEvent(pl.comm_stream, pl.ev_packed, 0));
+  rec(3, pl.comm_stream);
+  SHIRO_NCK(ncclGroupStart());
+  for (int k = 1; k < pl.P; ++k) {
+    // ring-shifted peer order: same schedule on every rank
+    const int d = (pl.rank + k) % pl.P, src = (pl.rank - k + pl.P) % pl.P;
+    const int64_t ns = pl.send_off[d + 1] - pl.send_off[d];
+    const int64_t nr = pl.recv_off[src + 1] - pl.recv_off[src];
+    if (ns) SHIRO_NCK(ncclSend(pl.send_buf + pl.send_off[d] * pl.N, (size_t)(ns * pl.N), ncclFloat,
+                               d, pl.comm, pl.comm_stream));
+    if (nr) SHIRO_NCK(ncclRecv(pl.recv_buf + pl.recv_off[src] * pl.N, (size_t)(nr * pl.N),
+                               ncclFloat, src, pl.comm, pl.comm_stream));
+  }
+  SHIRO_NCK(ncclGroupEnd());
+  rec(4, pl.comm_stream);
+  SHIRO_CK(cudaEventRecord(pl.ev_recvd, pl.comm_stream));
+  if (overlap) {
+    rec(5, s);
+    launches += stage_local(pl, B, C, s);
+    rec(6, s);
+  }
+  SHIRO_CK(cudaStreamWaitEvent(s, pl.ev_recvd, 0));
+  if (!overlap) {
+    rec(5, s);
+    launches += stage_local(pl, B, C, s);
+    rec(6, s);
+  }
+  if (pl.flags & SHIRO_F_FUSED_RECV) {
+    launches += run_spmm(pl.d_rem, pl.recv_buf, pl.recv_rows, nullptr, C, true, s);
+    rec(7, s);
+  } else {
+    launches += run_spmm(pl.d_col, pl.recv_buf, pl.recv_rows, nullptr, C, true, s);
+    rec(7, s);
+    launches += launch_scatter_add(pl.d_scatter.nt, pl.d_scatter.tgt, pl.d_scatter.ptr,
+                                   pl.d_scatter.src, pl.recv_buf, C, pl.N, s);
+  }
+  rec(8, s);
+  pl.last_launches = launches;
+  pl.prof_used = 2;
+}
+
+}  // namespace shiro
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using namespace shiro;
+
+struct shiro_plan_s {
+  bool loopback = false;
+  std::unique_ptr<Plan> single;                 // distributed: this rank
+  std::vector<std::unique_ptr<Plan>> ranks;     // loopback: all virtual ranks
+  std::vector<std::unique_ptr<shiro_plan_s>> views;
+  Plan *view = nullptr;                         // borrowed rank view
+  int64_t last_launches = 0;
+  Plan &rank_plan() { return view ? *view : *single; }
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(const Error &e) {
+  g_last_error = e.msg;
+  return e.code;
+}
+
+template <typename F>
+int guarded(F &&f) {
+  try {
+    g_last_error.clear();
+    f();
+    return SHIRO_OK;
+  } catch (const Error &e) {
+    return fail(e);
+  } catch (const std::bad_alloc &) {
+    return fail(Error(SHIRO_E_OOM, "host allocation failed"));
+  } catch (const std::exception &e) {
+    return fail(Error(SHIRO_E_INTERNAL, e.what()));
+  }
+}
+
+// NCCL all-to-allv of host byte segments (plan time only): sizes first.
+void nccl_host_alltoallv(ncclComm_t comm, int P, int rank, cudaStream_t s,
+                         const std::vector<std::vector<char>> &send,
+                         std::vector<std::vector<char>> &recv) {
+  std::vector<int64_t> ssz(P, 0), rsz(P, 0);
+  for (int p = 0; p < P; ++p) ssz[p] = p == rank ? 0 : (int64_t)send[p].size();
+  int64_t *d_sz = nullptr;
+  SHIRO_CK(cudaMalloc(&d_sz, 2 * P * sizeof(int64_t)));
+  SHIRO_CK(cudaMemcpyAsync(d_sz, ssz.data(), P * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  SHIRO_NCK(ncclGroupStart());
+  for (int p = 0; p < P; ++p) {
+    if (p == rank) continue;
+    SHIRO_NCK(ncclSend(d_sz + p, 8, ncclChar, p, comm, s));
+    SHIRO_NCK(ncclRecv(d_sz + P + p, 8, ncclChar, p, comm, s));
+  }
+  SHIRO_NCK(ncclGroupEnd());
+  SHIRO_CK(cudaMemcpyAsync(rsz.data(), d_sz + P, P * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  SHIRO_CK(cudaStreamSynchronize(s));
+  SHIRO_CK(cudaFree(d_sz));
+  rsz[rank] = 0;
+  std::vector<int64_t> so(P + 1, 0), ro(P + 1, 0);
+  for (int p = 0; p < P; ++p) { so[p + 1] = so[p] + ssz[p]; ro[p + 1] = ro[p] + rsz[p]; }
+  char *d_buf = nullptr;
+  SHIRO_CK(cudaMalloc(&d_buf, std::max<int64_t>(1, so[P] + ro[P])));
+  for (int p = 0; p < P; ++p)
+    if (ssz[p]) SHIRO_CK(cudaMemcpyAsync(d_buf + so[p], send[p].data(), ssz[p],
+                                         cudaMemcpyHostToDevice, s));
+  SHIRO_NCK(ncclGroupStart());
+  for (int p = 0; p < P; ++p) {
+    if (p == rank) continue;
+    if (ssz[p]) SHIRO_NCK(ncclSend(d_buf + so[p], ssz[p], ncclChar, p, comm, s));
+    if (rsz[p]) SHIRO_NCK(ncclRecv(d_buf + so[P] + ro[p], rsz[p], ncclChar, p, comm, s));
+  }
+  SHIRO_NCK(ncclGroupEnd());
+  recv.assign(P, {});
+  for (int p = 0; p < P; ++p) {
+    recv[p].resize(rsz[p]);
+    if (rsz[p]) SHIRO_CK(cudaMemcpyAsync(recv[p].data(), d_buf + so[P] + ro[p], rsz[p],
+                                         cudaMemcpyDeviceToHost, s));
+  }
+  SHIRO_CK(cudaStreamSynchronize(s));
+  SHIRO_CK(cudaFree(d_buf));
+}
+
+// Caller-provided host transport (e.g. gloo): sizes first, then payload.
+void callback_alltoallv(shiro_alltoallv_fn fn, void *ctx, int P, int rank,
+                        const std::vector<std::vector<char>> &send,
+                        std::vector<std::vector<char>> &recv) {
+  std::vector<int64_t> ssz(P, 0), rsz(P, 0), eight(P, 8);
+  for (int p = 0; p < P; ++p) ssz[p] = p == rank ? 0 : (int64_t)send[p].size();
+  eight[rank] = 8;
+  if (fn(ctx, ssz.data(), eight.data(), rsz.data(), eight.data()) != 0)
+    throw Error(SHIRO_E_TRANSPORT, "host transport failed (sizes)");
+  rsz[rank] = 0;
+  std::vector<char> sb, rb;
+  int64_t rt = 0;
+  for (int p = 0; p < P; ++p) {
+    if (p != rank) sb.insert(sb.end(), send[p].begin(), send[p].end());
+    rt += rsz[p];
+  }
+  ssz[rank] = 0;
+  rb.resize(std::max<int64_t>(rt, 1));
+  if (sb.empty()) sb.resize(1);
+  if (fn(ctx, sb.data(), ssz.data(), rb.data(), rsz.data()) != 0)
+    throw Error(SHIRO_E_TRANSPORT, "host transport failed (payload)");
+  recv.assign(P, {});
+  int64_t o = 0;
+  for (int p = 0; p < P; ++p) {
+    recv[p].assign(rb.begin() + o, rb.begin() + o + rsz[p]);
+    o += rsz[p];
+  }
+}
+
+// Status agreement before any payload exchange (every rank learns every
+// rank's validation status).
+int agree_status(const Alltoallv &x, int P, int rank, int mine) {
+  std::vector<std::vector<char>> send(P), recv;
+  for (int p = 0; p < P; ++p) {
+    send[p].resize(4);
+    std::memcpy(send[p].data(), &mine, 4);
+  }
+  x(send, recv);
+  int worst = mine;
+  for (int p = 0; p < P; ++p) {
+    if (p == rank) continue;
+    int v = 0;
+    if (recv[p].size() == 4) std::memcpy(&v, recv[p].data(), 4);
+    if (v != 0 && worst == 0) worst = SHIRO_E_PEER;
+  }
+  return worst;
+}
+
+void fill_block_stats(const Phase1 &p1, const PlanInput &in, Plan &pl) {
+  int64_t cols = 0, rows = 0, block = 0, setup = 0;
+  for (int q = 0; q < in.P; ++q) {
+    if (q == in.rank || p1.n_cols[q] == 0) continue;
+    cols += p1.n_cols[q];
+    rows += p1.n_rows[q];
+    block += in.part[q + 1] - in.part[q];
+    setup += 8 * p1.nnz_row[q];
+  }
+  pl.loc_cols = cols;
+  pl.loc_rows = rows;
+  pl.loc_block = block;
+  pl.loc_setup = setup;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *shiro_last_error(void) { return g_last_error.c_str(); }
+
+int shiro_get_unique_id(void *id128) {
+  return guarded([&] {
+    if (!id128) throw Error(SHIRO_E_ARG, "id buffer is NULL");
+    ncclUniqueId id;
+    SHIRO_NCK(ncclGetUniqueId(&id));
+    static_assert(sizeof(id) == 128, "ncclUniqueId must be 128 bytes");
+    std::memcpy(id128, &id, 128);
+  });
+}
+
+int shiro_plan(const shiro_dist_t *d, int64_t n, const int64_t *part, const int64_t *row_ptr,
+               const int32_t *col_idx, const float *val, int32_t N, void *stream,
+               shiro_plan_t *out) {
+  if (out) *out = nullptr;
+  return guarded([&] {
+    auto t0 = std::chrono::steady_clock::now();
+    if (!d || !out) throw Error(SHIRO_E_ARG, "dist/out is NULL");
+    const bool host_only = d->flags & SHIRO_F_HOST_ONLY;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    PlanInput in{d->rank, d->nranks, d->group_size, d->flags, n, part, row_ptr, col_idx, val, N};
+    if (d->nranks < 1 || d->rank < 0 || d->rank >= d->nranks)
+      throw Error(SHIRO_E_ARG, "bad rank/nranks");
+    auto h = std::make_unique<shiro_plan_s>();
+    h->single = std::make_unique<Plan>();
+    Plan &pl = *h->single;
+    // transport
+    Alltoallv xchg;
+    if (d->nranks > 1) {
+      if (d->host_xchg) {
+        xchg = [&](const std::vector<std::vector<char>> &snd, std::vector<std::vector<char>> &rcv) {
+          callback_alltoallv(d->host_xchg, d->host_xchg_ctx, d->nranks, d->rank, snd, rcv);
+        };
+      }
+      if (!host_only || !d->host_xchg) {
+        if (!d->nccl_id) throw Error(SHIRO_E_ARG, "nccl_id is NULL with nranks > 1");
+        ncclUniqueId id;
+        std::memcpy(&id, d->nccl_id, 128);
+        SHIRO_NCK(ncclCommInitRank(&pl.comm, d->nranks, id, d->rank));
+        if (!d->host_xchg) {
+          ncclComm_t comm = pl.comm;
+          int P = d->nranks, r = d->rank;
+          xchg = [comm, P, r, s](const std::vector<std::vector<char>> &snd,
+                                 std::vector<std::vector<char>> &rcv) {
+            nccl_host_alltoallv(comm, P, r, s, snd, rcv);
+          };
+        }
+      }
+    } else {
+      xchg = [](const std::vector<std::vector<char>> &snd, std::vector<std::vector<char>> &rcv) {
+        rcv.assign(snd.size(), {});
+      };
+    }
+    // P1: validate, then agree on the status across ranks
+    int st = 0;
+    std::string msg;
+    try {
+      validate_input(in);
+    } catch (const Error &e) {
+      st = e.code;
+      msg = e.msg;
+    }
+    if (d->nranks > 1) {
+      int agreed = agree_status(xchg, d->nranks, d->rank, st);
+      if (agreed != 0) throw Error(st ? st : agreed, st ? msg : "another rank failed validation");
+    } else if (st) {
+      throw Error(st, msg);
+    }
+    // P2-P3
+    Phase1 p1 = plan_phase1(in);
+    // P4: one-time exchange of lists + A_row
+    std::vector<std::vector<char>> in_msgs;
+    xchg(p1.out, in_msgs);
+    in_msgs.resize(d->nranks);
+    plan_phase2(in, p1, in_msgs, pl);
+    fill_block_stats(p1, in, pl);
+    plan_stats(in, pl, xchg);
+    if (!host_only) plan_upload(pl, s);
+    pl.info.plan_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *out = h.release();
+  });
+}
+
+int shiro_plan_loopback(int32_t nranks, int32_t group_size, uint32_t flags, int64_t n,
+                        const int64_t *part, const int64_t *row_ptr, const int32_t *col_idx,
+                        const float *val, int32_t N, void *stream, shiro_plan_t *out) {
+  if (out) *out = nullptr;
+  return guarded([&] {
+    auto t0 = std::chrono::steady_clock::now();
+    if (!out || !part || !row_ptr) throw Error(SHIRO_E_ARG, "NULL argument");
+    if (nranks < 1 || nranks > 64) throw Error(SHIRO_E_ARG, "nranks must be in 1..64");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool host_only = flags & SHIRO_F_HOST_ONLY;
+    const int P = nranks;
+    auto h = std::make_unique<shiro_plan_s>();
+    h->loopback = true;
+    std::vector<PlanInput> ins(P);
+    std::vector<std::vector<int64_t>> rps(P);
+    for (int r = 0; r < P; ++r) {
+      PlanInput in{r, P, group_size, flags, n, part, nullptr, nullptr, nullptr, N};
+      if (part[0] != 0 || part[P] != n) throw Error(SHIRO_E_PART, "part[0]/part[P] mismatch");
+      for (int p = 0; p < P; ++p)
+        if (part[p + 1] < part[p]) throw Error(SHIRO_E_PART, "part must be non-decreasing");
+      const int64_t lo = part[r], hi = part[r + 1], base = row_ptr[lo];
+      rps[r].resize(hi - lo + 1);
+      for (int64_t t = lo; t <= hi; ++t) rps[r][t - lo] = row_ptr[t] - base;
+      in.row_ptr = rps[r].data();
+      in.col = col_idx ? col_idx + base : nullptr;
+      in.val = val ? val + base : nullptr;
+      validate_input(in);
+      ins[r] = in;
+    }
+    std::vector<Phase1> p1(P);
+    for (int r = 0; r < P; ++r) p1[r] = plan_phase1(ins[r]);
+    // in-process exchange: message r -> q lands at q from r
+    std::vector<std::vector<std::vector<char>>> inbox(P, std::vector<std::vector<char>>(P));
+    for (int r = 0; r < P; ++r)
+      for (int q = 0; q < P; ++q)
+        if (q != r) inbox[q][r] = p1[r].out[q];
+    for (int r = 0; r < P; ++r) {
+      h->ranks.push_back(std::make_unique<Plan>());
+      Plan &pl = *h->ranks.back();
+      pl.loopback_view = false;
+      plan_phase2(ins[r], p1[r], inbox[r], pl);
+      fill_block_stats(p1[r], ins[r], pl);
+    }
+    // stats exchange among virtual ranks: run plan_stats sequentially with a
+    // transport that serves precomputed vectors (two passes)
+    std::vector<std::vector<char>> shares(P);
+    for (int r = 0; r < P; ++r) {
+      Alltoallv cap = [&, r](const std::vector<std::vector<char>> &snd,
+                             std::vector<std::vector<char>> &rcv) {
+        shares[r] = snd[(r + 1) % P];
+        rcv.assign(P, {});
+        for (int p = 0; p < P; ++p) rcv[p] = snd[(r + 1) % P];
+      };
+      plan_stats(ins[r], *h->ranks[r], cap);
+    }
+    for (int r = 0; r < P; ++r) {
+      Alltoallv serve = [&](const std::vector<std::vector<char>> &,
+                            std::vector<std::vector<char>> &rcv) {
+        rcv.assign(P, {});
+        for (int p = 0; p < P; ++p) rcv[p] = shares[p];
+      };
+      plan_stats(ins[r], *h->ranks[r], serve);
+    }
+    for (int r = 0; r < P; ++r) {
+      Plan &pl = *h->ranks[r];
+      if (!host_only) {
+        plan_upload(pl, s);
+      }
+      pl.info.plan_seconds =
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+    *out = h.release();
+  });
+}
+
+int shiro_plan_rank(shiro_plan_t plan, int32_t r, shiro_plan_t *out) {
+  return guarded([&] {
+    if (!plan || !out) throw Error(SHIRO_E_ARG, "NULL argument");
+    if (!plan->loopback) {
+      if (r != plan->single->rank) throw Error(SHIRO_E_ARG, "not this rank");
+      *out = plan;
+      return;
+    }
+    if (r < 0 || r >= (int)plan->ranks.size()) throw Error(SHIRO_E_ARG, "rank out of range");
+    if (plan->views.empty())
+      for (auto &p : plan->ranks) {
+        auto v = std::make_unique<shiro_plan_s>();
+        v->view = p.get();
+        plan->views.push_back(std::move(v));
+      }
+    *out = plan->views[r].get();
+  });
+}
+
+int shiro_spmm(shiro_plan_t plan, const float *B_p, float *C_p, void *stream) {
+  return guarded([&] {
+    if (!plan || plan->loopback || plan->view) throw Error(SHIRO_E_ARG, "not a distributed plan");
+    Plan &pl = *plan->single;
+    if (!pl.arena) throw Error(SHIRO_E_ARG, "plan was built with SHIRO_F_HOST_ONLY");
+    if (pl.M > 0 && (!B_p || !C_p)) throw Error(SHIRO_E_ARG, "B/C is NULL");
+    if (pl.comm) {
+      ncclResult_t as = ncclSuccess;
+      ncclCommGetAsyncError(pl.comm, &as);
+      if (as != ncclSuccess && as != ncclInProgress)
+        throw Error(SHIRO_E_NCCL, std::string("asynchronous NCCL error: ") + ncclGetErrorString(as));
+    }
+    exec_flat(pl, B_p, C_p, static_cast<cudaStream_t>(stream));
+    SHIRO_CK(cudaGetLastError());
+    plan->last_launches = pl.last_launches;
+  });
+}
+
+int shiro_spmm_host(shiro_plan_t plan, const float *B_host, float *C_host, void *stream) {
+  return guarded([&] {
+    if (!plan || plan->loopback || plan->view) throw Error(SHIRO_E_ARG, "not a distributed plan");
+    Plan &pl = *plan->single;
+    if (!pl.arena) throw Error(SHIRO_E_ARG, "plan was built with SHIRO_F_HOST_ONLY");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t bytes = (size_t)pl.M * pl.N * sizeof(float);
+    if (!pl.stage && bytes) SHIRO_CK(cudaMalloc(&pl.stage, 2 * bytes));   // once per plan
+    float *dB = pl.stage, *dC = pl.stage ? pl.stage + (size_t)pl.M * pl.N : nullptr;
+    if (bytes) SHIRO_CK(cudaMemcpyAsync(dB, B_host, bytes, cudaMemcpyHostToDevice, s));
+    exec_flat(pl, dB, dC, s);
+    if (bytes) SHIRO_CK(cudaMemcpyAsync(C_host, dC, bytes, cudaMemcpyDeviceToHost, s));
+    SHIRO_CK(cudaStreamSynchronize(s));
+    plan->last_launches = pl.last_launches;
+  });
+}
+
+int shiro_spmm_loopback(shiro_plan_t plan, const float *B, float *C, void *stream) {
+  return guarded([&] {
+    if (!plan || !plan->loopback) throw Error(SHIRO_E_ARG, "not a loopback plan");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int P = (int)plan->ranks.size();
+    int64_t launches = 0;
+    for (auto &p : plan->ranks)
+      if (!p->arena) throw Error(SHIRO_E_ARG, "plan was built with SHIRO_F_HOST_ONLY");
+    const int N = plan->ranks[0]->N;
+    auto Bp = [&](int r) { return B + plan->ranks[r]->part[r] * N; };
+    auto Cp = [&](int r) { return C + plan->ranks[r]->part[r] * N; };
+    if (P == 1) {
+      launches += stage_local(*plan->ranks[0], Bp(0), Cp(0), s);
+    } else {
+      for (int r = 0; r < P; ++r) launches += stage_send(*plan->ranks[r], Bp(r), s);
+      // exchange: device copies send(s -> r) into recv(r from s)
+      for (int r = 0; r < P; ++r) {
+        Plan &dst = *plan->ranks[r];
+        for (int src = 0; src < P; ++src) {
+          if (src == r) continue;
+          Plan &sp = *plan->ranks[src];
+          const int64_t rows = sp.send_off[r + 1] - sp.send_off[r];
+          if (rows != dst.recv_off[src + 1] - dst.recv_off[src])
+            throw Error(SHIRO_E_INTERNAL, "loopback segment size mismatch");
+          if (rows)
+            SHIRO_CK(cudaMemcpyAsync(dst.recv_buf + dst.recv_off[src] * N,
+                                     sp.send_buf + sp.send_off[r] * N,
+                                     (size_t)rows * N * sizeof(float), cudaMemcpyDeviceToDevice, s));
+        }
+      }
+      for (int r = 0; r < P; ++r) {
+        launches += stage_local(*plan->ranks[r], Bp(r), Cp(r), s);
+        launches += stage_recv(*plan->ranks[r], Cp(r), s);
+      }
+    }
+    SHIRO_CK(cudaGetLastError());
+    plan->last_launches = launches;
+  });
+}
+
+int shiro_free(shiro_plan_t plan) {
+  return guarded([&] {
+    if (!plan) return;
+    if (plan->view) throw Error(SHIRO_E_ARG, "cannot free a borrowed rank view");
+    delete plan;
+  });
+}
+
+int shiro_plan_info(shiro_plan_t plan, shiro_info_t *out) {
+  return guarded([&] {
+    if (!plan || !out) throw Error(SHIRO_E_ARG, "NULL argument");
+    if (plan->loopback) {
+      *out = plan->ranks[0]->info;
+      int64_t dev = 0;
+      for (auto &p : plan->ranks) dev += p->info.dev_bytes;
+      out->dev_bytes = dev;
+      return;
+    }
+    *out = plan->rank_plan().info;
+  });
+}
+
+int shiro_plan_list(shiro_plan_t plan, int32_t peer, int32_t kind, int64_t *buf, int64_t cap,
+                    int64_t *len) {
+  return guarded([&] {
+    if (!plan || !len) throw Error(SHIRO_E_ARG, "NULL argument");
+    if (plan->loopback && !plan->view) throw Error(SHIRO_E_ARG, "use shiro_plan_rank first");
+    Plan &pl = plan->rank_plan();
+    if (peer < 0 || peer >= pl.P) throw Error(SHIRO_E_ARG, "peer out of range");
+    const std::vector<int64_t> *v = nullptr;
+    switch (kind) {
+      case SHIRO_LIST_SEND_B: v = &pl.send_b[peer]; break;
+      case SHIRO_LIST_SEND_C: v = &pl.send_c[peer]; break;
+      case SHIRO_LIST_RECV_B: v = &pl.recv_b[peer]; break;
+      case SHIRO_LIST_RECV_C: v = &pl.recv_c[peer]; break;
+      default: throw Error(SHIRO_E_ARG, "unknown list kind");
+    }
+    *len = (int64_t)v->size();
+    if (buf) std::memcpy(buf, v->data(), sizeof(int64_t) * std::min<int64_t>(cap, *len));
+  });
+}
+
+int shiro_profile(shiro_plan_t plan, int32_t enable) {
+  return guarded([&] {
+    if (!plan || plan->loopback || plan->view) throw Error(SHIRO_E_ARG, "not a distributed plan");
+    Plan &pl = *plan->single;
+    if (enable && !pl.prof[0])
+      for (auto &e : pl.prof) SHIRO_CK(cudaEventCreate(&e));
+    pl.prof_on = enable != 0;
+    pl.prof_used = 0;
+  });
+}
+
+int shiro_stage_times(shiro_plan_t plan, double *ms) {
+  return guarded([&] {
+    if (!plan || !ms || plan->loopback || plan->view) throw Error(SHIRO_E_ARG, "bad argument");
+    Plan &pl = *plan->single;
+    for (int i = 0; i < SHIRO_NUM_STAGES; ++i) ms[i] = 0.0;
+    if (!pl.prof_on || !pl.prof_used) throw Error(SHIRO_E_ARG, "no profiled call");
+    auto el = [&](int a, int b) {
+      float t = 0.f;
+      SHIRO_CK(cudaEventSynchronize(pl.prof[b]));
+      SHIRO_CK(cudaEventElapsedTime(&t, pl.prof[a], pl.prof[b]));
+      return (double)t;
+    };
+    if (pl.prof_used == 1) {
+      ms[SHIRO_STAGE_LOCAL] = ms[SHIRO_STAGE_TOTAL] = el(5, 6);
+      return;
+    }
+    ms[SHIRO_STAGE_PACK] = el(0, 1);
+    ms[SHIRO_STAGE_PARTIAL] = el(1, 2);
+    ms[SHIRO_STAGE_EXCHANGE] = el(3, 4);
+    ms[SHIRO_STAGE_LOCAL] = el(5, 6);
+    if (pl.flags & SHIRO_F_NO_OVERLAP) {
+      ms[SHIRO_STAGE_REMOTE] = el(6, 7);
+    } else {
+      // remote starts when both the local SpMM and the exchange are done
+      const double t_local_end = el(0, 6), t_x_end = el(0, 4);
+      ms[SHIRO_STAGE_REMOTE] = el(0, 7) - std::max(t_local_end, t_x_end);
+    }
+    ms[SHIRO_STAGE_SCATTER] = el(7, 8);
+    ms[SHIRO_STAGE_TOTAL] = el(0, 8);
+  });
+}
+
+int64_t shiro_last_launches(shiro_plan_t plan) { return plan ? plan->last_launches : -1; }
+
+}  // extern "C"

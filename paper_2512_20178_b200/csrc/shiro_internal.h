@@ -1,0 +1,159 @@
+// shiro_internal.h -- host-side structures of the planner and executor.
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "../../include/shiro.h"
+#include "kernels.h"
+
+namespace shiro {
+
+struct Error {
+  int code;
+  std::string msg;
+  Error(int c, std::string m) : code(c), msg(std::move(m)) {}
+};
+
+#define SHIRO_CK(x)                                                                      \
+  do {                                                                                   \
+    cudaError_t e_ = (x);                                                                \
+    if (e_ != cudaSuccess)                                                               \
+      throw ::shiro::Error(e_ == cudaErrorMemoryAllocation ? SHIRO_E_OOM : SHIRO_E_CUDA, \
+                           std::string(#x) + ": " + cudaGetErrorString(e_));             \
+  } while (0)
+
+#define SHIRO_NCK(x)                                                                     \
+  do {                                                                                   \
+    ncclResult_t r_ = (x);                                                               \
+    if (r_ != ncclSuccess)                                                               \
+      throw ::shiro::Error(SHIRO_E_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+// canonical block cover (cover.cpp); returns mu
+int64_t block_cover(int32_t nr, int32_t nc, const std::vector<int64_t> &ap,
+                    const std::vector<int32_t> &adj, bool colmax, std::vector<uint8_t> &sel_row,
+                    std::vector<uint8_t> &sel_col);
+
+// vector shape of width N (kernels.cu); false -> generic path
+bool vec_shape_public(int N, int *lpr, int *vpl);
+
+// Host CSR of one SpMM op.  out_row empty = identity.
+struct HostCsr {
+  int64_t nrows = 0;
+  std::vector<int64_t> rp{0};
+  std::vector<int32_t> col;
+  std::vector<float> val;       // empty = all ones
+  std::vector<int32_t> out_row;
+  int64_t nnz() const { return (int64_t)col.size(); }
+};
+
+// Device image of a SpMM op (arrays live in the plan's arena)
+struct DevSpmm {
+  SpmmArgs a;            // pointers to device arrays; X/Y filled at run time
+  int64_t nnz = 0;
+};
+
+// Device image of a gather (pack) or gather-sum (scatter) op
+struct DevPack {
+  int64_t n = 0;
+  const int32_t *src = nullptr, *dst = nullptr;
+};
+struct DevScatter {
+  int64_t nt = 0;
+  const int32_t *tgt = nullptr;
+  const int64_t *ptr = nullptr;
+  const int32_t *src = nullptr;
+  int64_t nsrc = 0;
+};
+
+// Plan-time transport: collective all-to-allv of host byte segments.
+using Alltoallv = std::function<void(const std::vector<std::vector<char>> &send,
+                                     std::vector<std::vector<char>> &recv)>;
+
+struct Plan {
+  // identity
+  int32_t rank = 0, P = 1, g = 1;
+  uint32_t flags = 0;
+  int64_t n = 0;
+  int32_t N = 0;
+  std::vector<int64_t> part;
+  int64_t M = 0;            // local rows (= local B rows)
+  int device = 0;
+  bool loopback_view = false;
+
+  // lists, global ids ascending, indexed by peer
+  std::vector<std::vector<int64_t>> send_b, send_c, recv_b, recv_c;
+  std::vector<int64_t> send_off, recv_off;   // rows, [P+1]
+  int64_t send_rows = 0, recv_rows = 0;
+
+  // hierarchical stage lists (group_size > 1): per stage, per peer
+  std::vector<std::vector<int64_t>> h_send[2], h_recv[2];
+
+  // host images of the ops
+  HostCsr A_diag, A_out, A_col, A_rem;
+  std::vector<int32_t> pack_src, pack_dst;
+  std::vector<int32_t> sc_tgt, sc_src;
+  std::vector<int64_t> sc_ptr{0};
+
+  // stats
+  shiro_info_t info{};
+  int64_t loc_cols = 0, loc_rows = 0, loc_block = 0, loc_setup = 0;   // owned blocks
+
+  // device state
+  void *arena = nullptr;
+  size_t arena_bytes = 0;
+  float *send_buf = nullptr, *recv_buf = nullptr;
+  DevSpmm d_diag, d_out, d_col, d_rem;
+  DevPack d_pack;
+  DevScatter d_scatter;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_packed = nullptr, ev_recvd = nullptr;
+  ncclComm_t comm = nullptr;
+  int64_t last_launches = 0;
+  // stage profiling (shiro_profile)
+  bool prof_on = false;
+  cudaEvent_t prof[12] = {};
+  int prof_used = 0;
+  // device staging of B and C for shiro_spmm_host
+  float *stage = nullptr;
+
+  ~Plan();
+};
+
+struct PlanInput {
+  int32_t rank, P, g;
+  uint32_t flags;
+  int64_t n;
+  const int64_t *part;
+  const int64_t *row_ptr;   // this rank's rows
+  const int32_t *col;
+  const float *val;
+  int32_t N;
+};
+
+// planner phases (plan.cpp)
+void validate_input(const PlanInput &in);
+// phase 1: covers of the owned blocks -> outgoing messages per peer
+struct Phase1 {
+  std::vector<std::vector<char>> out;             // message to each peer
+  std::vector<int8_t> tag;                        // per local nonzero: 0 local, 1 row, 2 col
+  std::vector<std::vector<int64_t>> recv_b, recv_c;   // what each q sends us
+  std::vector<int64_t> n_rows, n_cols, nnz_row;       // per q: |Rows|, |Cols| of A^(p,q)
+};
+Phase1 plan_phase1(const PlanInput &in);
+void plan_phase2(const PlanInput &in, Phase1 &p1, const std::vector<std::vector<char>> &in_msgs,
+                 Plan &plan);
+// global statistics (needs one more all-to-allv)
+void plan_stats(const PlanInput &in, Plan &plan, const Alltoallv &xchg);
+// device upload
+void plan_upload(Plan &plan, cudaStream_t s);
+
+// executor (runtime.cpp)
+void exec_flat(Plan &plan, const float *B, float *C, cudaStream_t s);
+
+}  // namespace shiro
