@@ -125,6 +125,44 @@ def traffic_from_profiles(config, world, op):
     return d.get(f"{config}/P{world}/{op}")
 
 
+def gather_probes(sh, torch, dev, stream, Bd, rp_l, col_l, lo, hi, N, flush, reps=5):
+    if N not in (32, 64, 128):
+        return None
+    res = {}
+
+    def timeit(X, idx):
+        out = torch.empty(((idx.numel() + 255) // 256, N), device=dev)
+        sh.probe_gather(X, idx, out, 256, stream)
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            sh.probe_gather(X, idx, out, 256, stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms = float(np.median(ts))
+        return ms, idx.numel() * N * 4 / (ms * 1e-3) / 1e9
+
+    # the local SpMM's own diagonal-block column stream (CSR order)
+    c = np.asarray(col_l, np.int64)
+    keep = (c >= lo) & (c < hi)
+    idx = torch.from_numpy((c[keep] - lo).astype(np.int32)).to(dev)
+    if idx.numel():
+        ms, gbs = timeit(Bd, idx)
+        res["csr_stream_ms"] = round(ms, 5)
+        res["csr_stream_gbs"] = round(gbs, 1)
+    g = torch.Generator(device="cpu").manual_seed(0)
+    n_idx = 1 << 22
+    for name, rows in (("l2_random_gbs", (32 << 20) // (4 * N)), ("hbm_random_gbs", (4 << 30) // (4 * N))):
+        X = torch.ones((rows, N), device=dev)
+        ridx = torch.randint(0, rows, (n_idx,), generator=g, dtype=torch.int32).to(dev)
+        res[name] = round(timeit(X, ridx)[1], 1)
+        del X
+    return res
+
+
 # ----------------------------------------------------------------- reference arm
 def run_reference(args, cfg, world, rank):
     """The oracle (as it stands) on the host cores: each step computes the
@@ -322,6 +360,14 @@ def main():
             "peak_source": peaks["source"],
             "gather_bytes": int(4 * cfg.N * info["op_nnz"][dom]) if dom != "pack" else None}
 
+    # gather-aware roofline: the dominant local op's own column stream through
+    # the pure gather probe, plus uniform-random gathers from an L2-resident
+    # (32 MiB) and an HBM-resident (4 GiB) table
+    gather = gather_probes(sh, torch, dev, stream, Bd, rp_l, col_l, lo, hi, cfg.N, flush)
+    if gather and dom == "local":
+        roof["gather_floor_ms"] = gather["csr_stream_ms"]
+        roof["gather_frac"] = round(gather["csr_stream_ms"] / dom_ms, 4)
+
     # exchange (NVLink) achieved bandwidth, per rank max(send, recv) bytes
     xbytes = 4 * cfg.N * max(info["send_b_rows"] + info["send_c_rows"],
                              info["recv_b_rows"] + info["recv_c_rows"])
@@ -389,6 +435,7 @@ def main():
                       if info["g_oblivious_rows"] else None,
                       "setup_bytes": info["g_setup_bytes"]},
             "exchange": exch,
+            "gather_probe": gather,
             "stages_ms": {k: round(v, 5) for k, v in stage_ms.items()},
             "step_ms": {"median": round(float(np.median(step_ms)), 5),
                         "p10": round(float(np.percentile(step_ms, 10)), 5),

@@ -211,6 +211,13 @@ int shiro_plan_rank(shiro_plan_t plan, int32_t r, shiro_plan_t *out);
 int shiro_profile(shiro_plan_t plan, int32_t enable);
 int shiro_stage_times(shiro_plan_t plan, double *ms /* [SHIRO_NUM_STAGES] */);
 
+/* Measurement probe (not on the hot path): out[c] = sum of the rows
+ * X[idx[k]] over chunks c of `chunk` consecutive indices (out: ceil(n/chunk)
+ * x N).  Device pointers; N in {32, 64, 128}.  Timing it on an SpMM's own
+ * column-index stream gives that SpMM's gather-aware roofline. */
+int shiro_probe_gather(const float *X, int32_t N, const int32_t *idx, int64_t n_idx, float *out,
+                       int32_t chunk, void *stream);
+
 /* Number of kernel launches the last shiro_spmm* issued on this plan (all
  * virtual ranks for loopback), NCCL kernels excluded. */
 int64_t shiro_last_launches(shiro_plan_t plan);

@@ -96,6 +96,7 @@ def load():
         "shiro_plan_rank": [P, I32, ctypes.POINTER(P)],
         "shiro_profile": [P, I32],
         "shiro_stage_times": [P, P],
+        "shiro_probe_gather": [P, I32, P, I64, P, I32, P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -125,6 +126,13 @@ def _stream_ptr(stream):
     if isinstance(stream, int):
         return ctypes.c_void_p(stream)
     return ctypes.c_void_p(stream.cuda_stream)
+
+
+def probe_gather(X, idx, out, chunk=256, stream=None):
+    """shiro_probe_gather on torch CUDA tensors (X fp32 [*, N], idx int32)."""
+    _check(load().shiro_probe_gather(ctypes.c_void_p(X.data_ptr()), X.shape[1],
+                                     ctypes.c_void_p(idx.data_ptr()), idx.numel(),
+                                     ctypes.c_void_p(out.data_ptr()), chunk, _stream_ptr(stream)))
 
 
 def get_unique_id() -> bytes:

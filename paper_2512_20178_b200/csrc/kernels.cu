@@ -3,20 +3,25 @@
 // The dense width N of B and C is the contraction-free axis of SpMM: every
 // nonzero a_ij contributes a length-N axpy of row j of the source into row i
 // of the output.  The work is a memory-bound gather, so
-// the kernels are designed around HBM3e / L2 traffic, not tensor cores:
-//   * a row of the source is N*4 bytes (512 B at N = 128); a group of
-//     LPR = min(32, N/4) lanes owns one output row and moves it with 128-bit
-//     loads (float4) -- one fully coalesced LDG.128 per lane per nonzero;
-//   * the row's (col, val) pairs are loaded cooperatively (one pair per lane,
-//     streamed with L1::no_allocate) and broadcast with shuffles, then U = 8
-//     independent row gathers are issued before any FMA (memory-level
-//     parallelism for short power-law rows);
-//   * accumulation is fp32 in registers, one store per output row;
-//   * rows longer than L nonzeros (hubs) are split into chunk tasks that run
-//     first; their partials are reduced in chunk order by the last-arriving
-//     chunk (threadfence + arrival counter): deterministic, single launch.
+// the kernels are designed around L2 / HBM3e traffic, not tensor cores:
+//   * a source row is N*4 bytes (512 B at N = 128); a group of
+//     LPR = min(32, N/4) lanes owns one output row and moves each source row
+//     with one 128-bit load per lane (fully coalesced LDG.128);
+//   * the nonzeros of a work unit are loaded cooperatively as interleaved
+//     (col, val) pairs, one 8-byte streaming load per lane, and broadcast with
+//     shuffles; U = 8 independent row gathers are issued before any FMA;
+//   * short rows are packed at plan time into row groups (<= L nonzeros,
+//     <= 64 rows); a per-nonzero byte gives the row offset inside the group,
+//     so row boundaries cost no memory access and the gathers of many short
+//     rows stay in flight together; empty rows are written as zeros;
+//   * rows longer than L nonzeros (power-law hubs) become chunk tasks of L
+//     nonzeros scheduled first; their partials are reduced in chunk order by
+//     the last-arriving chunk (threadfence + arrival counter): deterministic,
+//     single launch;
+//   * fp32 accumulation in registers, one store per output row.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "kernels.h"
 
@@ -25,19 +30,19 @@ namespace shiro {
 namespace {
 
 constexpr int kBlock = 256;   // 8 warps per CTA
-constexpr int kUnroll = 8;    // outstanding row gathers per lane group
 
-__device__ __forceinline__ int ld_stream_i32(const int32_t *p) {
-  int v;
-  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+__device__ __forceinline__ int2 ld_stream_cv(const int2 *p) {
+  int2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.s32 {%0, %1}, [%2];"
+               : "=r"(v.x), "=r"(v.y)
+               : "l"(p));
   return v;
 }
-__device__ __forceinline__ float ld_stream_f32(const float *p) {
-  float v;
-  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
-  return v;
+__device__ __forceinline__ int ld_stream_u8(const uint8_t *p) {
+  unsigned short v;
+  asm volatile("ld.global.nc.L1::no_allocate.u8 %0, [%1];" : "=h"(v) : "l"(p));
+  return (int)v;
 }
-__device__ __forceinline__ int64_t ld_i64(const int64_t *p) { return __ldg(p); }
 
 __device__ __forceinline__ void fma4(float4 &acc, float v, const float4 &x) {
   acc.x = fmaf(v, x.x, acc.x);
@@ -49,62 +54,39 @@ __device__ __forceinline__ void add4(float4 &acc, const float4 &x) {
   acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
 }
 
-// Source row pointer in the unified row space [X0 || X1].
+// Source row in the unified row space [X0 || X1] (X1 unused when n0 covers all).
+template <bool TWO>
 __device__ __forceinline__ const float4 *src_row(const SpmmArgs &a, int c) {
-  const float *base = (c < a.n0) ? a.X0 + (int64_t)c * a.N : a.X1 + (int64_t)(c - a.n0) * a.N;
-  return reinterpret_cast<const float4 *>(base);
+  if (TWO && c >= a.n0) return reinterpret_cast<const float4 *>(a.X1 + (int64_t)(c - a.n0) * a.N);
+  return reinterpret_cast<const float4 *>(a.X0 + (int64_t)c * a.N);
 }
 
-// acc[v] += sum_{k in [kb, ke)} val[k] * X(col[k])[(li + v*LPR)*4 .. +3]
-template <int LPR, int VPL>
-__device__ __forceinline__ void accum_range(float4 (&acc)[VPL], const SpmmArgs &a, int64_t kb,
-                                            int64_t ke, int li, unsigned mask) {
-  constexpr int U = (LPR < kUnroll) ? LPR : kUnroll;
-  for (int64_t base = kb; base < ke; base += LPR) {
-    const int64_t k = base + li;
-    int c = 0;
-    float v = 0.f;
-    if (k < ke) {
-      c = ld_stream_i32(a.col + k);
-      v = a.val ? ld_stream_f32(a.val + k) : 1.f;
-    }
-    const int cnt = (int)((ke - base) < LPR ? (ke - base) : LPR);
-    for (int j = 0; j < cnt; j += U) {
-      float4 x[U][VPL];
-      float w[U];
+// Gather U source rows for nonzeros j..j+U-1 of the current batch; the
+// weights are broadcast together with the columns, before any FMA.
+template <int LPR, int VPL, bool TWO, int U>
+__device__ __forceinline__ void gather(const SpmmArgs &a, float4 (&x)[U][VPL], float (&w)[U],
+                                       int c, float v, int j, int cnt, int li, unsigned mask) {
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int cu = __shfl_sync(mask, c, j + u, LPR);
-        const float vu = __shfl_sync(mask, v, j + u, LPR);
-        if (j + u < cnt) {            // uniform across the lane group
-          const float4 *r = src_row(a, cu);
+  for (int u = 0; u < U; ++u) {
+    const int cu = __shfl_sync(mask, c, j + u, LPR);
+    const float vu = __shfl_sync(mask, v, j + u, LPR);
+    if (j + u < cnt) {               // uniform across the lane group
+      const float4 *r = src_row<TWO>(a, cu);
 #pragma unroll
-          for (int q = 0; q < VPL; ++q) x[u][q] = __ldg(r + li + q * LPR);
-          w[u] = vu;
-        } else {
+      for (int q = 0; q < VPL; ++q) x[u][q] = __ldg(r + li + q * LPR);
+      w[u] = vu;
+    } else {
 #pragma unroll
-          for (int q = 0; q < VPL; ++q) x[u][q] = make_float4(0.f, 0.f, 0.f, 0.f);
-          w[u] = 0.f;
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int q = 0; q < VPL; ++q) fma4(acc[q], w[u], x[u][q]);
+      for (int q = 0; q < VPL; ++q) x[u][q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      w[u] = 0.f;
     }
   }
 }
 
-template <int LPR, int VPL, bool ACCUM>
-__global__ void __launch_bounds__(kBlock) k_spmm(const SpmmArgs a) {
-  constexpr int R = 32 / LPR;   // output rows per warp
-  const int lane = threadIdx.x & 31;
-  const int sub = lane / LPR;
-  const int li = lane % LPR;
-  const unsigned mask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (sub * LPR));
-  const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
-  const int64_t u = warp * R + sub;     // work unit: chunk task, then regular row
-
+// One work unit u: a chunk task (u < n_tasks) or a row group.
+template <int LPR, int VPL, bool ACCUM, bool TWO, int U>
+__device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, const int li,
+                                          const unsigned mask) {
   float4 acc[VPL];
 #pragma unroll
   for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -114,10 +96,24 @@ __global__ void __launch_bounds__(kBlock) k_spmm(const SpmmArgs a) {
     const int lr = a.task_long[u];
     const int64_t t = a.long_row[lr];
     const int f = a.long_first[lr], nch = a.long_first[lr + 1] - f;
-    const int64_t rb = ld_i64(a.rp + t), re = ld_i64(a.rp + t + 1);
+    const int64_t rb = __ldg(a.rp + t), re = __ldg(a.rp + t + 1);
     const int64_t kb = rb + (int64_t)(u - f) * a.L;
     const int64_t ke = (kb + a.L < re) ? kb + a.L : re;
-    accum_range<LPR, VPL>(acc, a, kb, ke, li, mask);
+    for (int64_t base = kb; base < ke; base += LPR) {
+      const int64_t k = base + li;
+      int2 cv = make_int2(0, 0);
+      if (k < ke) cv = ld_stream_cv(a.cv + k);
+      const int cnt = (int)((ke - base) < LPR ? (ke - base) : LPR);
+      for (int j = 0; j < cnt; j += U) {
+        float4 x[U][VPL];
+        float w[U];
+        gather<LPR, VPL, TWO, U>(a, x, w, cv.x, __int_as_float(cv.y), j, cnt, li, mask);
+#pragma unroll
+        for (int uu = 0; uu < U; ++uu)
+#pragma unroll
+          for (int q = 0; q < VPL; ++q) fma4(acc[q], w[uu], x[uu][q]);
+      }
+    }
     float4 *sp = reinterpret_cast<float4 *>(a.scratch + u * (int64_t)a.N);
 #pragma unroll
     for (int q = 0; q < VPL; ++q) __stcg(sp + li + q * LPR, acc[q]);
@@ -140,33 +136,84 @@ __global__ void __launch_bounds__(kBlock) k_spmm(const SpmmArgs a) {
       float4 *y = reinterpret_cast<float4 *>(a.Y + orow * a.N);
 #pragma unroll
       for (int q = 0; q < VPL; ++q) {
-        if (ACCUM) {
-          float4 o = y[li + q * LPR];
-          add4(o, s[q]);
-          s[q] = o;
-        }
+        if (ACCUM) add4(s[q], y[li + q * LPR]);
         y[li + q * LPR] = s[q];
       }
       if (li == 0) a.long_counter[lr] = 0;    // re-arm for the next launch
     }
     return;
   }
-  const int64_t t = u - a.n_tasks;
-  if (t >= a.nrows) return;
-  const int64_t kb = ld_i64(a.rp + t), ke = ld_i64(a.rp + t + 1);
-  if (ke - kb > a.L) return;              // handled by chunk tasks
-  accum_range<LPR, VPL>(acc, a, kb, ke, li, mask);
-  const int64_t orow = a.out_row ? a.out_row[t] : t;
-  float4 *y = reinterpret_cast<float4 *>(a.Y + orow * a.N);
-#pragma unroll
-  for (int q = 0; q < VPL; ++q) {
-    if (ACCUM) add4(acc[q], y[li + q * LPR]);
-    y[li + q * LPR] = acc[q];
+
+  // ---- row group: rows [r0, r1), nonzeros [k0, k1) ------------------------
+  const int64_t gi = u - a.n_tasks;
+  if (gi >= a.n_groups) return;
+  const RowGroup g = a.groups[gi];
+  const int nrows = g.r1 - g.r0;
+  // output rows of the group, one per lane (groups with an out_row map have
+  // <= 2*LPR rows, checked at plan time)
+  int orw0 = 0, orw1 = 0;
+  if (a.out_row) {
+    if (li < nrows) orw0 = __ldg(a.out_row + g.r0 + li);
+    if (LPR + li < nrows) orw1 = __ldg(a.out_row + g.r0 + LPR + li);
   }
+  int cur = 0;   // current row offset inside the group
+  auto flush = [&]() {
+    int64_t orow;
+    if (a.out_row) {
+      const int sel = (cur < LPR) ? orw0 : orw1;
+      orow = __shfl_sync(mask, sel, cur & (LPR - 1), LPR);
+    } else {
+      orow = g.r0 + cur;
+    }
+    float4 *y = reinterpret_cast<float4 *>(a.Y + orow * a.N);
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) {
+      if (ACCUM) add4(acc[q], y[li + q * LPR]);
+      y[li + q * LPR] = acc[q];
+      acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    ++cur;
+  };
+  for (int64_t base = g.k0; base < g.k1; base += LPR) {
+    const int64_t k = base + li;
+    int2 cv = make_int2(0, 0);
+    int ro = 0;
+    if (k < g.k1) {
+      cv = ld_stream_cv(a.cv + k);
+      ro = ld_stream_u8(a.roff + k);
+    }
+    const int cnt = (int)((g.k1 - base) < LPR ? (g.k1 - base) : LPR);
+    for (int j = 0; j < cnt; j += U) {
+      float4 x[U][VPL];
+      float w[U];
+      gather<LPR, VPL, TWO, U>(a, x, w, cv.x, __int_as_float(cv.y), j, cnt, li, mask);
+#pragma unroll
+      for (int uu = 0; uu < U; ++uu) {
+        const int rou = __shfl_sync(mask, ro, j + uu, LPR);
+        if (j + uu < cnt) {
+          while (cur < rou) flush();        // finished rows (and empty rows)
+#pragma unroll
+          for (int q = 0; q < VPL; ++q) fma4(acc[q], w[uu], x[uu][q]);
+        }
+      }
+    }
+  }
+  while (cur < nrows) flush();              // last row and trailing empty rows
 }
 
-// Generic width (N % 4 != 0 or N not a supported vector width): one warp per
-// row, lanes stride over columns; no row splitting.  Correctness path.
+template <int LPR, int VPL, bool ACCUM, bool TWO, int MINB, int U>
+__global__ void __launch_bounds__(kBlock, MINB) k_spmm(const SpmmArgs a) {
+  constexpr int R = 32 / LPR;   // lane groups per warp
+  const int lane = threadIdx.x & 31;
+  const int sub = lane / LPR;
+  const int li = lane % LPR;
+  const unsigned mask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (sub * LPR));
+  const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  spmm_unit<LPR, VPL, ACCUM, TWO, (U < LPR ? U : LPR)>(a, warp * R + sub, li, mask);
+}
+
+// Generic width (N not a supported vector width): one warp per CSR row,
+// lanes stride over columns; no row grouping or splitting.  Correctness path.
 template <bool ACCUM>
 __global__ void __launch_bounds__(kBlock) k_spmm_generic(const SpmmArgs a) {
   const int lane = threadIdx.x & 31;
@@ -178,8 +225,9 @@ __global__ void __launch_bounds__(kBlock) k_spmm_generic(const SpmmArgs a) {
   for (int c0 = 0; c0 < a.N; c0 += 32 * 4) {
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
     for (int64_t k = kb; k < ke; ++k) {
-      const int c = a.col[k];
-      const float v = a.val ? a.val[k] : 1.f;
+      const int2 cv = a.cv[k];
+      const int c = cv.x;
+      const float v = __int_as_float(cv.y);
       const float *r = (c < a.n0) ? a.X0 + (int64_t)c * a.N : a.X1 + (int64_t)(c - a.n0) * a.N;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -236,6 +284,9 @@ __global__ void __launch_bounds__(kBlock) k_pack_generic(int64_t n, const int32_
   for (int x = lane; x < N; x += 32) d[x] = s[x];
 }
 
+// K5: gather-sum of received partial C rows.  One lane group owns a target
+// row: C[t] = C[t] + sum of its partials in source order (at most P-1 flat,
+// plus hierarchical aggregates) -- no atomics, deterministic.
 template <int LPR, int VPL>
 __global__ void __launch_bounds__(kBlock) k_scatter_add(int64_t nt, const int32_t *__restrict__ tgt,
                                                         const int64_t *__restrict__ ptr,
@@ -253,8 +304,6 @@ __global__ void __launch_bounds__(kBlock) k_scatter_add(int64_t nt, const int32_
   float4 acc[VPL];
 #pragma unroll
   for (int q = 0; q < VPL; ++q) acc[q] = c[li + q * LPR];
-  // at most P-1 partials per row (plus hierarchical aggregates): load all
-  // partial rows of a chunk of 4 before adding, in source order
   for (int64_t k = kb; k < ke; k += 4) {
     float4 x[4][VPL];
 #pragma unroll
@@ -292,34 +341,48 @@ __global__ void __launch_bounds__(kBlock) k_scatter_add_generic(int64_t nt, cons
   }
 }
 
-// Vector shape for width N: LPR lanes per row, VPL float4 per lane.
-bool vec_shape(int N, int *lpr, int *vpl) {
-  switch (N) {
-    case 4: *lpr = 1; *vpl = 1; return true;
-    case 8: *lpr = 2; *vpl = 1; return true;
-    case 16: *lpr = 4; *vpl = 1; return true;
-    case 32: *lpr = 8; *vpl = 1; return true;
-    case 64: *lpr = 16; *vpl = 1; return true;
-    case 128: *lpr = 32; *vpl = 1; return true;
-    case 256: *lpr = 32; *vpl = 2; return true;
-    case 512: *lpr = 32; *vpl = 4; return true;
-    default: return false;
-  }
-}
-
 inline int64_t blocks_for(int64_t units, int rows_per_warp) {
   const int64_t per_block = (int64_t)(kBlock / 32) * rows_per_warp;
   return (units + per_block - 1) / per_block;
 }
 
+template <int LPR, int VPL, int MINB, int U>
+void spmm_launch(const SpmmArgs &a, bool acc, cudaStream_t s) {
+  const int64_t units = a.n_tasks + a.n_groups;
+  const unsigned grid = (unsigned)blocks_for(units, 32 / LPR);
+  const bool two = a.X1 != nullptr;
+  if (acc) {
+    if (two) k_spmm<LPR, VPL, true, true, MINB, U><<<grid, kBlock, 0, s>>>(a);
+    else k_spmm<LPR, VPL, true, false, MINB, U><<<grid, kBlock, 0, s>>>(a);
+  } else {
+    if (two) k_spmm<LPR, VPL, false, true, MINB, U><<<grid, kBlock, 0, s>>>(a);
+    else k_spmm<LPR, VPL, false, false, MINB, U><<<grid, kBlock, 0, s>>>(a);
+  }
+}
+
+// Kernel variant: (resident CTAs per SM requested from ptxas, gather depth U).
+// SHIRO_KVAR selects one for tuning sweeps; the default is the measured best.
+int spmm_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("SHIRO_KVAR");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 template <int LPR, int VPL>
 void spmm_shape(const SpmmArgs &a, bool acc, cudaStream_t s) {
-  const int64_t units = a.n_tasks + a.nrows;
-  const int64_t grid = blocks_for(units, 32 / LPR);
-  if (acc)
-    k_spmm<LPR, VPL, true><<<(unsigned)grid, kBlock, 0, s>>>(a);
-  else
-    k_spmm<LPR, VPL, false><<<(unsigned)grid, kBlock, 0, s>>>(a);
+  if (VPL > 1) { spmm_launch<LPR, VPL, 1, 8>(a, acc, s); return; }
+  switch (spmm_variant()) {
+    case 1: spmm_launch<LPR, VPL, 3, 8>(a, acc, s); break;
+    case 2: spmm_launch<LPR, VPL, 4, 8>(a, acc, s); break;
+    case 3: spmm_launch<LPR, VPL, 4, 4>(a, acc, s); break;
+    case 4: spmm_launch<LPR, VPL, 5, 4>(a, acc, s); break;
+    case 5: spmm_launch<LPR, VPL, 6, 4>(a, acc, s); break;
+    case 6: spmm_launch<LPR, VPL, 2, 16>(a, acc, s); break;
+    default: spmm_launch<LPR, VPL, 1, 8>(a, acc, s); break;
+  }
 }
 
 template <int LPR, int VPL>
@@ -352,7 +415,20 @@ void scatter_shape(int64_t nt, const int32_t *tgt, const int64_t *ptr, const int
 
 }  // namespace
 
-bool vec_shape_public(int N, int *lpr, int *vpl) { return vec_shape(N, lpr, vpl); }
+// Vector shape for width N: LPR lanes per row, VPL float4 per lane.
+bool vec_shape(int N, int *lpr, int *vpl) {
+  switch (N) {
+    case 4: *lpr = 1; *vpl = 1; return true;
+    case 8: *lpr = 2; *vpl = 1; return true;
+    case 16: *lpr = 4; *vpl = 1; return true;
+    case 32: *lpr = 8; *vpl = 1; return true;
+    case 64: *lpr = 16; *vpl = 1; return true;
+    case 128: *lpr = 32; *vpl = 1; return true;
+    case 256: *lpr = 32; *vpl = 2; return true;
+    case 512: *lpr = 32; *vpl = 4; return true;
+    default: return false;
+  }
+}
 
 int num_sms() {
   static int n = 0;
@@ -366,9 +442,10 @@ int num_sms() {
 }
 
 int launch_spmm(const SpmmArgs &a, bool accumulate, cudaStream_t s) {
-  if (a.nrows == 0 && a.n_tasks == 0) return 0;
+  if (a.nrows == 0) return 0;
   int lpr, vpl;
   if (vec_shape(a.N, &lpr, &vpl)) {
+    if (a.n_tasks + a.n_groups == 0) return 0;
     SHIRO_DISPATCH(a.N, spmm_shape, a, accumulate, s);
   } else {
     const int64_t grid = blocks_for(a.nrows, 1);

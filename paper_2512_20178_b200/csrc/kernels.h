@@ -12,20 +12,30 @@ namespace shiro {
 // out_row == nullptr means out_row[t] = t.  Rows with more than L nonzeros
 // are split into chunk tasks of L nonzeros (power-law hub rows); the chunk
 // partials are reduced in a fixed order by the last-arriving chunk, so the
-// result is deterministic.
+// result is deterministic.  All other rows are packed into row groups of at
+// most ~L nonzeros (plan time); one lane group streams a whole group, so the
+// gathers of consecutive short rows are in flight together.
+// A row group: consecutive short rows [r0, r1) whose nonzeros are [k0, k1).
+struct RowGroup {
+  int64_t k0, k1;
+  int32_t r0, r1;
+};
+
 struct SpmmArgs {
   int64_t nrows = 0;
-  const int64_t *rp = nullptr;
-  const int32_t *col = nullptr;
-  const float *val = nullptr;
+  const int64_t *rp = nullptr;          // [nrows+1]
+  const int2 *cv = nullptr;             // [nnz] interleaved (column, value bits)
+  const uint8_t *roff = nullptr;        // [nnz] row offset inside its row group
   const int32_t *out_row = nullptr;
   const float *X0 = nullptr;
   int64_t n0 = 0;
   const float *X1 = nullptr;
   float *Y = nullptr;
   int32_t N = 0;
-  int32_t L = 0x7fffffff;         // split threshold
-  int32_t n_tasks = 0;            // chunk tasks (long rows)
+  int32_t L = 0x7fffffff;               // long-row threshold = chunk size
+  int32_t n_groups = 0;
+  const RowGroup *groups = nullptr;     // [n_groups]
+  int32_t n_tasks = 0;                  // chunk tasks (long rows)
   const int32_t *task_long = nullptr;   // [n_tasks] long-row index of each task
   const int32_t *long_row = nullptr;    // [n_long] CSR row t of each long row
   const int32_t *long_first = nullptr;  // [n_long+1] first task of each long row
@@ -48,5 +58,9 @@ int launch_scatter_add(int64_t nt, const int32_t *tgt, const int64_t *ptr, const
 
 // SM count of the current device (cached)
 int num_sms();
+
+// vector shape of width N: LPR lanes per row, VPL float4 per lane; false ->
+// generic (scalar) path
+bool vec_shape(int N, int *lpr, int *vpl);
 
 }  // namespace shiro

@@ -54,55 +54,79 @@ size_t put(Arena &ar, const std::vector<T> &v) {
   return ar.reserve(v.size() * sizeof(T), v.empty() ? nullptr : v.data());
 }
 
-// Row-split threshold L for one op: hub rows are cut into chunks of L
-// nonzeros so that no single lane group holds the tail (power-law inputs).
-int32_t split_threshold(int64_t nnz) {
-  int64_t L = nnz / ((int64_t)num_sms() * 64);
-  L = std::max<int64_t>(128, std::min<int64_t>(4096, L));
-  return (int32_t)L;
-}
+// Work decomposition of one SpMM op (plan time).  Rows with more than L
+// nonzeros (power-law hubs) become chunk tasks of L nonzeros; every other row
+// belongs to a row group: a run of consecutive short rows with at most L
+// nonzeros and kMaxGroupRows rows (2*LPR when an out_row map is used),
+// streamed by one lane group; a per-nonzero byte holds the row offset inside
+// the group.
+constexpr int32_t kChunk = 256;
+constexpr int32_t kMaxGroupRows = 64;
 
 struct SplitHost {
   int32_t L = 0x7fffffff;
   std::vector<int32_t> task_long, long_row, long_first{0};
+  std::vector<RowGroup> groups;
+  std::vector<uint8_t> roff;
+  std::vector<int2> cv;
 };
 
 SplitHost make_split(const HostCsr &c, int N) {
   SplitHost s;
+  s.cv.resize(c.nnz());
+  for (int64_t k = 0; k < c.nnz(); ++k) {
+    const float v = c.val.empty() ? 1.0f : c.val[k];
+    int bits;
+    std::memcpy(&bits, &v, 4);
+    s.cv[k] = make_int2(c.col[k], bits);
+  }
   int lpr, vpl;
-  if (!vec_shape_public(N, &lpr, &vpl)) return s;   // generic path: no split
-  s.L = split_threshold(c.nnz());
-  for (int64_t t = 0; t < c.nrows; ++t) {
-    const int64_t d = c.rp[t + 1] - c.rp[t];
-    if (d > s.L) {
+  if (!vec_shape(N, &lpr, &vpl)) return s;   // generic path: row per warp
+  s.L = kChunk;
+  s.roff.assign(c.nnz(), 0);
+  const int64_t max_rows = c.out_row.empty() ? kMaxGroupRows : std::min(kMaxGroupRows, 2 * lpr);
+  auto deg = [&](int64_t r) { return c.rp[r + 1] - c.rp[r]; };
+  int64_t t = 0;
+  while (t < c.nrows) {
+    if (deg(t) > s.L) {
       const int32_t lr = (int32_t)s.long_row.size();
       s.long_row.push_back((int32_t)t);
-      const int64_t nch = (d + s.L - 1) / s.L;
+      const int64_t nch = (deg(t) + s.L - 1) / s.L;
       for (int64_t k = 0; k < nch; ++k) s.task_long.push_back(lr);
       s.long_first.push_back((int32_t)s.task_long.size());
+      ++t;
+      continue;
     }
+    const int64_t r0 = t;
+    int64_t sum = 0;
+    while (t < c.nrows && deg(t) <= s.L && t - r0 < max_rows && (t == r0 || sum + deg(t) <= s.L)) {
+      for (int64_t k = c.rp[t]; k < c.rp[t + 1]; ++k) s.roff[k] = (uint8_t)(t - r0);
+      sum += deg(t);
+      ++t;
+    }
+    s.groups.push_back(RowGroup{c.rp[r0], c.rp[t], (int32_t)r0, (int32_t)t});
   }
   return s;
 }
 
 struct SpmmLayout {
-  size_t rp, col, val, out, tl, lrow, lfirst, cnt, scratch;
+  size_t rp, cv, roff, out, tl, lrow, lfirst, cnt, scratch, grp;
   SplitHost sp;
-  bool has_val, has_out;
+  bool has_out;
 };
 
 SpmmLayout layout_spmm(Arena &ar, const HostCsr &c, int N) {
   SpmmLayout L;
   L.sp = make_split(c, N);
   L.rp = put(ar, c.rp);
-  L.col = put(ar, c.col);
-  L.has_val = !c.val.empty();
+  L.cv = put(ar, L.sp.cv);
+  L.roff = put(ar, L.sp.roff);
   L.has_out = !c.out_row.empty();
-  L.val = put(ar, c.val);
   L.out = put(ar, c.out_row);
   L.tl = put(ar, L.sp.task_long);
   L.lrow = put(ar, L.sp.long_row);
   L.lfirst = put(ar, L.sp.long_first);
+  L.grp = put(ar, L.sp.groups);
   L.cnt = ar.reserve(L.sp.long_row.size() * sizeof(int32_t));          // zeroed
   L.scratch = ar.reserve(L.sp.task_long.size() * (size_t)N * sizeof(float));
   return L;
@@ -113,12 +137,14 @@ DevSpmm bind_spmm(char *base, const SpmmLayout &L, const HostCsr &c, int N) {
   SpmmArgs &a = d.a;
   a.nrows = c.nrows;
   a.rp = reinterpret_cast<const int64_t *>(base + L.rp);
-  a.col = reinterpret_cast<const int32_t *>(base + L.col);
-  a.val = L.has_val ? reinterpret_cast<const float *>(base + L.val) : nullptr;
+  a.cv = reinterpret_cast<const int2 *>(base + L.cv);
+  a.roff = reinterpret_cast<const uint8_t *>(base + L.roff);
   a.out_row = L.has_out ? reinterpret_cast<const int32_t *>(base + L.out) : nullptr;
   a.N = N;
   a.L = L.sp.L;
   a.n_tasks = (int32_t)L.sp.task_long.size();
+  a.n_groups = (int32_t)L.sp.groups.size();
+  a.groups = reinterpret_cast<const RowGroup *>(base + L.grp);
   a.task_long = reinterpret_cast<const int32_t *>(base + L.tl);
   a.long_row = reinterpret_cast<const int32_t *>(base + L.lrow);
   a.long_first = reinterpret_cast<const int32_t *>(base + L.lfirst);

@@ -39,8 +39,6 @@ int64_t block_cover(int32_t nr, int32_t nc, const std::vector<int64_t> &ap,
                     const std::vector<int32_t> &adj, bool colmax, std::vector<uint8_t> &sel_row,
                     std::vector<uint8_t> &sel_col);
 
-// vector shape of width N (kernels.cu); false -> generic path
-bool vec_shape_public(int N, int *lpr, int *vpl);
 
 // Host CSR of one SpMM op.  out_row empty = identity.
 struct HostCsr {
