@@ -248,6 +248,8 @@ def main():
     ap.add_argument("--fused", action="store_true", help="SHIRO_F_FUSED_RECV")
     ap.add_argument("--colmax", action="store_true", help="SHIRO_F_COVER_COLMAX")
     ap.add_argument("--mode", default="joint", choices=["joint", "col", "row"])
+    ap.add_argument("--xchg", default="p2p", choices=["p2p", "nccl"],
+                    help="fused NVLink exchange (default) or NCCL grouped send/recv")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -291,6 +293,8 @@ def main():
     if args.colmax:
         flags |= sh.F_COVER_COLMAX
     flags |= {"joint": 0, "col": sh.F_MODE_COL, "row": sh.F_MODE_ROW}[args.mode]
+    if args.xchg == "nccl":
+        flags |= sh.F_XCHG_NCCL
     nccl_id = None
     if world > 1:
         obj = [sh.get_unique_id() if rank == 0 else None]
@@ -420,7 +424,8 @@ def main():
                                (" col-max" if args.colmax else " row-max"),
                        "partition": "uniform 1D rows (larger blocks first)",
                        "l2": "flushed (256 MiB memset) before every timed step",
-                       "parallelism": f"1D row partition over {world} rank(s), NCCL all-to-allv"},
+                       "exchange": (args.xchg if world > 1 else "none"),
+                       "parallelism": f"1D row partition over {world} rank(s)"},
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,

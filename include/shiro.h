@@ -67,6 +67,10 @@ enum shiro_status {
 #define SHIRO_F_FUSED_RECV (1u << 3)   /* remote SpMM + scatter-add in one pass  */
 #define SHIRO_F_HOST_ONLY (1u << 4)    /* plan lists/stats only, no device state */
 #define SHIRO_F_NO_OVERLAP (1u << 5)   /* local SpMM after the exchange (ablation)*/
+#define SHIRO_F_XCHG_NCCL (1u << 6)    /* exchange with NCCL grouped send/recv
+                                          instead of the default fused exchange
+                                          (K4/K3 store straight into the peers'
+                                          receive buffers over NVLink, CUDA IPC) */
 
 /* list kinds for shiro_plan_list */
 #define SHIRO_LIST_SEND_B 0 /* B rows this rank sends to `peer` (global ids)     */

@@ -28,6 +28,7 @@ F_MODE_ROW = 1 << 2
 F_FUSED_RECV = 1 << 3
 F_HOST_ONLY = 1 << 4
 F_NO_OVERLAP = 1 << 5
+F_XCHG_NCCL = 1 << 6
 
 STAGES = ("pack", "partial", "exchange", "local", "remote", "scatter", "total")
 

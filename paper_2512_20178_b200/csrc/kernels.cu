@@ -83,8 +83,10 @@ __device__ __forceinline__ void gather(const SpmmArgs &a, float4 (&x)[U][VPL], f
   }
 }
 
-// One work unit u: a chunk task (u < n_tasks) or a row group.
-template <int LPR, int VPL, bool ACCUM, bool TWO, int U>
+// One work unit u: a chunk task (u < n_tasks) or a row group.  OUTP: output
+// rows are addressed by a per-row pointer (e.g. a peer's receive buffer over
+// NVLink, the fused exchange) instead of Y + out_row * N.
+template <int LPR, int VPL, bool ACCUM, bool TWO, int U, bool OUTP>
 __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, const int li,
                                           const unsigned mask) {
   float4 acc[VPL];
@@ -132,8 +134,13 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
 #pragma unroll
         for (int q = 0; q < VPL; ++q) add4(s[q], __ldcg(cp + li + q * LPR));
       }
-      const int64_t orow = a.out_row ? a.out_row[t] : t;
-      float4 *y = reinterpret_cast<float4 *>(a.Y + orow * a.N);
+      float4 *y;
+      if (OUTP) {
+        y = reinterpret_cast<float4 *>(a.out_ptr[t]);
+      } else {
+        const int64_t orow = a.out_row ? a.out_row[t] : t;
+        y = reinterpret_cast<float4 *>(a.Y + orow * a.N);
+      }
 #pragma unroll
       for (int q = 0; q < VPL; ++q) {
         if (ACCUM) add4(s[q], y[li + q * LPR]);
@@ -152,20 +159,30 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
   // output rows of the group, one per lane (groups with an out_row map have
   // <= 2*LPR rows, checked at plan time)
   int orw0 = 0, orw1 = 0;
-  if (a.out_row) {
+  long long opw0 = 0, opw1 = 0;
+  if (OUTP) {
+    if (li < nrows) opw0 = (long long)a.out_ptr[g.r0 + li];
+    if (LPR + li < nrows) opw1 = (long long)a.out_ptr[g.r0 + LPR + li];
+  } else if (a.out_row) {
     if (li < nrows) orw0 = __ldg(a.out_row + g.r0 + li);
     if (LPR + li < nrows) orw1 = __ldg(a.out_row + g.r0 + LPR + li);
   }
   int cur = 0;   // current row offset inside the group
   auto flush = [&]() {
-    int64_t orow;
-    if (a.out_row) {
-      const int sel = (cur < LPR) ? orw0 : orw1;
-      orow = __shfl_sync(mask, sel, cur & (LPR - 1), LPR);
+    float4 *y;
+    if (OUTP) {
+      const long long sel = (cur < LPR) ? opw0 : opw1;
+      y = reinterpret_cast<float4 *>(__shfl_sync(mask, sel, cur & (LPR - 1), LPR));
     } else {
-      orow = g.r0 + cur;
+      int64_t orow;
+      if (a.out_row) {
+        const int sel = (cur < LPR) ? orw0 : orw1;
+        orow = __shfl_sync(mask, sel, cur & (LPR - 1), LPR);
+      } else {
+        orow = g.r0 + cur;
+      }
+      y = reinterpret_cast<float4 *>(a.Y + orow * a.N);
     }
-    float4 *y = reinterpret_cast<float4 *>(a.Y + orow * a.N);
 #pragma unroll
     for (int q = 0; q < VPL; ++q) {
       if (ACCUM) add4(acc[q], y[li + q * LPR]);
@@ -201,7 +218,7 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
   while (cur < nrows) flush();              // last row and trailing empty rows
 }
 
-template <int LPR, int VPL, bool ACCUM, bool TWO, int MINB, int U>
+template <int LPR, int VPL, bool ACCUM, bool TWO, int MINB, int U, bool OUTP>
 __global__ void __launch_bounds__(kBlock, MINB) k_spmm(const SpmmArgs a) {
   constexpr int R = 32 / LPR;   // lane groups per warp
   const int lane = threadIdx.x & 31;
@@ -209,7 +226,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmm(const SpmmArgs a) {
   const int li = lane % LPR;
   const unsigned mask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (sub * LPR));
   const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
-  spmm_unit<LPR, VPL, ACCUM, TWO, (U < LPR ? U : LPR)>(a, warp * R + sub, li, mask);
+  spmm_unit<LPR, VPL, ACCUM, TWO, (U < LPR ? U : LPR), OUTP>(a, warp * R + sub, li, mask);
 }
 
 // Generic width (N not a supported vector width): one warp per CSR row,
@@ -271,6 +288,47 @@ __global__ void __launch_bounds__(kBlock) k_pack(int64_t n, const int32_t *__res
       for (int q = 0; q < VPL; ++q) d[li + q * LPR] = x[r][q];
     }
   }
+}
+
+// K4 into peer buffers: Y row of packed row i is the pointer dstp[i].
+template <int LPR, int VPL>
+__global__ void __launch_bounds__(kBlock) k_pack_ptr(int64_t n, const int32_t *__restrict__ src,
+                                                     float *const *__restrict__ dstp,
+                                                     const float *__restrict__ X, int N) {
+  constexpr int R = 32 / LPR;
+  constexpr int RPU = 4;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane / LPR, li = lane % LPR;
+  const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const int64_t u0 = (warp * R + sub) * RPU;
+  float4 x[RPU][VPL];
+#pragma unroll
+  for (int r = 0; r < RPU; ++r) {
+    if (u0 + r < n) {
+      const float4 *s = reinterpret_cast<const float4 *>(X + (int64_t)__ldg(src + u0 + r) * N);
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) x[r][q] = __ldg(s + li + q * LPR);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RPU; ++r) {
+    if (u0 + r < n) {
+      float4 *d = reinterpret_cast<float4 *>(dstp[u0 + r]);
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) d[li + q * LPR] = x[r][q];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k_pack_ptr_generic(int64_t n, const int32_t *src,
+                                                             float *const *dstp, const float *X,
+                                                             int N) {
+  const int lane = threadIdx.x & 31;
+  const int64_t u = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  if (u >= n) return;
+  const float *s = X + (int64_t)src[u] * N;
+  float *d = dstp[u];
+  for (int x = lane; x < N; x += 32) d[x] = s[x];
 }
 
 __global__ void __launch_bounds__(kBlock) k_pack_generic(int64_t n, const int32_t *src,
@@ -351,12 +409,14 @@ void spmm_launch(const SpmmArgs &a, bool acc, cudaStream_t s) {
   const int64_t units = a.n_tasks + a.n_groups;
   const unsigned grid = (unsigned)blocks_for(units, 32 / LPR);
   const bool two = a.X1 != nullptr;
-  if (acc) {
-    if (two) k_spmm<LPR, VPL, true, true, MINB, U><<<grid, kBlock, 0, s>>>(a);
-    else k_spmm<LPR, VPL, true, false, MINB, U><<<grid, kBlock, 0, s>>>(a);
+  if (a.out_ptr) {   // fused exchange: overwrite rows in peer buffers
+    k_spmm<LPR, VPL, false, false, MINB, U, true><<<grid, kBlock, 0, s>>>(a);
+  } else if (acc) {
+    if (two) k_spmm<LPR, VPL, true, true, MINB, U, false><<<grid, kBlock, 0, s>>>(a);
+    else k_spmm<LPR, VPL, true, false, MINB, U, false><<<grid, kBlock, 0, s>>>(a);
   } else {
-    if (two) k_spmm<LPR, VPL, false, true, MINB, U><<<grid, kBlock, 0, s>>>(a);
-    else k_spmm<LPR, VPL, false, false, MINB, U><<<grid, kBlock, 0, s>>>(a);
+    if (two) k_spmm<LPR, VPL, false, true, MINB, U, false><<<grid, kBlock, 0, s>>>(a);
+    else k_spmm<LPR, VPL, false, false, MINB, U, false><<<grid, kBlock, 0, s>>>(a);
   }
 }
 
@@ -390,6 +450,13 @@ void pack_shape(int64_t n, const int32_t *src, const int32_t *dst, const float *
                 int N, cudaStream_t s) {
   const int64_t grid = blocks_for((n + 3) / 4, 32 / LPR);
   k_pack<LPR, VPL><<<(unsigned)grid, kBlock, 0, s>>>(n, src, dst, X, Y, N);
+}
+
+template <int LPR, int VPL>
+void pack_ptr_shape(int64_t n, const int32_t *src, float *const *dstp, const float *X, int N,
+                    cudaStream_t s) {
+  const int64_t grid = blocks_for((n + 3) / 4, 32 / LPR);
+  k_pack_ptr<LPR, VPL><<<(unsigned)grid, kBlock, 0, s>>>(n, src, dstp, X, N);
 }
 
 template <int LPR, int VPL>
@@ -465,6 +532,18 @@ int launch_pack(int64_t n, const int32_t *src, const int32_t *dst, const float *
     SHIRO_DISPATCH(N, pack_shape, n, src, dst, X, Y, N, s);
   } else {
     k_pack_generic<<<(unsigned)blocks_for(n, 1), kBlock, 0, s>>>(n, src, dst, X, Y, N);
+  }
+  return 1;
+}
+
+int launch_pack_ptr(int64_t n, const int32_t *src, float *const *dstp, const float *X, int32_t N,
+                    cudaStream_t s) {
+  if (n == 0) return 0;
+  int lpr, vpl;
+  if (vec_shape(N, &lpr, &vpl)) {
+    SHIRO_DISPATCH(N, pack_ptr_shape, n, src, dstp, X, N, s);
+  } else {
+    k_pack_ptr_generic<<<(unsigned)blocks_for(n, 1), kBlock, 0, s>>>(n, src, dstp, X, N);
   }
   return 1;
 }

@@ -27,6 +27,7 @@ struct SpmmArgs {
   const int2 *cv = nullptr;             // [nnz] interleaved (column, value bits)
   const uint8_t *roff = nullptr;        // [nnz] row offset inside its row group
   const int32_t *out_row = nullptr;
+  float *const *out_ptr = nullptr;      // per-row output address (fused exchange)
   const float *X0 = nullptr;
   int64_t n0 = 0;
   const float *X1 = nullptr;
@@ -50,6 +51,18 @@ int launch_spmm(const SpmmArgs &a, bool accumulate, cudaStream_t s);
 // K4: Y[dst[i]] = X[src[i]] for i < n (gather B rows into the send buffer)
 int launch_pack(int64_t n, const int32_t *src, const int32_t *dst, const float *X, float *Y,
                 int32_t N, cudaStream_t s);
+
+// K4 into peer memory: dstp[i] is the (peer-mapped) address of packed row i
+int launch_pack_ptr(int64_t n, const int32_t *src, float *const *dstp, const float *X, int32_t N,
+                    cudaStream_t s);
+
+// Fused-exchange synchronisation over NVLink (p2p.cu).  signal: for each i,
+// st.release.sys *flags[i] = value (flags[i] may be a peer address).  wait:
+// spin until every local flags[i] >= value (ld.acquire.sys); after
+// timeout_ns sets *err = 1 and gives up instead of hanging the GPU.
+int launch_signal(int32_t *const *flags, int n, int32_t value, cudaStream_t s);
+int launch_wait(const int32_t *flags, int n, int32_t value, int32_t *err, int64_t timeout_ns,
+                cudaStream_t s);
 
 // K5: C[tgt[u]] += sum_{k in [ptr[u], ptr[u+1])} R[src[k]] (gather-sum of
 // received partial C rows, fixed order: C first, then sources ascending)

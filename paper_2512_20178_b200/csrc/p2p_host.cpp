@@ -1,0 +1,137 @@
+// p2p_host.cpp -- setup of the fused NVLink exchange (collective, plan time).
+//
+// Every rank exports its plan arena (receive buffer + flags) with
+// cudaIpcGetMemHandle and sends to each peer the handle, the byte offsets of
+// its receive buffer and flags inside the arena, and the row offset at which
+// that peer's rows land in its receive buffer (recv_off).  Each rank then
+// opens the peers' arenas and precomputes, for every row it sends, the
+// peer-mapped destination address: K4 (pack) and K3 (row-based partial SpMM)
+// store straight into the receivers' buffers over NVLink -- the exchange is
+// fused into the producing kernels (workflow steps 3-4).
+// If any rank fails to map a peer, every rank keeps the NCCL exchange.
+#include <climits>
+#include <cstring>
+
+#include "shiro_internal.h"
+
+namespace shiro {
+
+namespace {
+
+struct PeerMsg {
+  cudaIpcMemHandle_t handle;
+  int64_t recv_buf_off, flags_off, recv_row_off;
+};
+
+template <typename T>
+std::vector<char> bytes_of(const T &x) {
+  std::vector<char> b(sizeof(T));
+  std::memcpy(b.data(), &x, sizeof(T));
+  return b;
+}
+
+}  // namespace
+
+void p2p_release(Plan &pl) {
+  for (void *b : pl.peer_base)
+    if (b) cudaIpcCloseMemHandle(b);
+  pl.peer_base.clear();
+  if (pl.p2p_arena) cudaFree(pl.p2p_arena);
+  pl.p2p_arena = nullptr;
+  if (pl.err_host) cudaFreeHost(pl.err_host);
+  pl.err_host = nullptr;
+  pl.p2p = false;
+}
+
+void p2p_setup(Plan &pl, const Alltoallv &xchg) {
+  const int P = pl.P, me = pl.rank;
+  const int64_t rowb = (int64_t)pl.N * sizeof(float);
+  // 1. export
+  cudaIpcMemHandle_t h;
+  int status = cudaIpcGetMemHandle(&h, pl.arena) == cudaSuccess ? 0 : 1;
+  std::vector<std::vector<char>> send(P), recv;
+  for (int d = 0; d < P; ++d) {
+    PeerMsg m{h, pl.recv_buf_off, pl.flags_off, pl.recv_off[d]};
+    send[d] = bytes_of(m);
+  }
+  xchg(send, recv);
+  // 2. open the peers' arenas
+  pl.peer_base.assign(P, nullptr);
+  std::vector<PeerMsg> pm(P);
+  for (int d = 0; d < P && status == 0; ++d) {
+    if (d == me) continue;
+    if (recv[d].size() != sizeof(PeerMsg)) { status = 1; break; }
+    std::memcpy(&pm[d], recv[d].data(), sizeof(PeerMsg));
+    void *base = nullptr;
+    if (cudaIpcOpenMemHandle(&base, pm[d].handle, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      status = 1;
+      break;
+    }
+    pl.peer_base[d] = base;
+  }
+  // 3. agree: all ranks use the fused exchange or none does
+  std::vector<std::vector<char>> st_send(P, bytes_of(status)), st_recv;
+  xchg(st_send, st_recv);
+  int any = status;
+  for (int d = 0; d < P; ++d)
+    if (d != me && st_recv[d].size() == sizeof(int)) {
+      int v;
+      std::memcpy(&v, st_recv[d].data(), sizeof(int));
+      any |= v;
+    }
+  if (any) {
+    p2p_release(pl);
+    return;   // NCCL exchange stays in place
+  }
+  // 4. destination addresses of every row this rank sends
+  auto peer_recv = [&](int d) {
+    return reinterpret_cast<char *>(pl.peer_base[d]) + pm[d].recv_buf_off;
+  };
+  std::vector<uint64_t> dstp, outp, rdy, cons;
+  for (int d = 0; d < P; ++d) {
+    if (d == me) continue;
+    char *base = peer_recv(d) + pm[d].recv_row_off * rowb;
+    for (size_t k = 0; k < pl.send_b[d].size(); ++k)
+      dstp.push_back((uint64_t)(base + (int64_t)k * rowb));
+    const int64_t nb = (int64_t)pl.send_b[d].size();
+    for (size_t k = 0; k < pl.send_c[d].size(); ++k)
+      outp.push_back((uint64_t)(base + (nb + (int64_t)k) * rowb));
+    char *fl = reinterpret_cast<char *>(pl.peer_base[d]) + pm[d].flags_off;
+    rdy.push_back((uint64_t)(fl + sizeof(int32_t) * me));
+    cons.push_back((uint64_t)(fl + sizeof(int32_t) * (P + me)));
+  }
+  if ((int64_t)outp.size() != pl.d_out.a.nrows || (int64_t)dstp.size() != pl.d_pack.n)
+    throw Error(SHIRO_E_INTERNAL, "fused exchange: row count mismatch");
+  const size_t n_all = dstp.size() + outp.size() + rdy.size() + cons.size();
+  SHIRO_CK(cudaMalloc(&pl.p2p_arena, std::max<size_t>(8, n_all * sizeof(uint64_t))));
+  uint64_t *a = static_cast<uint64_t *>(pl.p2p_arena);
+  std::vector<uint64_t> all;
+  all.insert(all.end(), dstp.begin(), dstp.end());
+  all.insert(all.end(), outp.begin(), outp.end());
+  all.insert(all.end(), rdy.begin(), rdy.end());
+  all.insert(all.end(), cons.begin(), cons.end());
+  if (!all.empty())
+    SHIRO_CK(cudaMemcpy(a, all.data(), all.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  pl.pack_dstp = reinterpret_cast<float *const *>(a);
+  pl.d_out_p2p = pl.d_out;
+  pl.d_out_p2p.a.out_ptr = reinterpret_cast<float *const *>(a + dstp.size());
+  pl.ready_ptrs = reinterpret_cast<int32_t *const *>(a + dstp.size() + outp.size());
+  pl.consumed_ptrs = reinterpret_cast<int32_t *const *>(a + dstp.size() + outp.size() + rdy.size());
+  // 5. local flags: own entries never block (INT_MAX), the rest start at 0
+  std::vector<int32_t> f(2 * P + 1, 0);
+  f[me] = INT_MAX;
+  f[P + me] = INT_MAX;
+  SHIRO_CK(cudaMemcpy(pl.xflags, f.data(), f.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  SHIRO_CK(cudaMallocHost(&pl.err_host, sizeof(int32_t)));
+  *pl.err_host = 0;
+  if (const char *e = getenv("SHIRO_P2P_TIMEOUT_MS")) pl.wait_timeout_ns = atoll(e) * 1000000LL;
+  pl.epoch = 0;
+  pl.p2p = true;
+  // every rank's flags are initialised before any peer signals into them
+  std::vector<std::vector<char>> bar_send(P, bytes_of(0)), bar_recv;
+  SHIRO_CK(cudaDeviceSynchronize());
+  xchg(bar_send, bar_recv);
+}
+
+}  // namespace shiro

@@ -23,6 +23,7 @@ namespace shiro {
 
 Plan::~Plan() {
   if (!loopback_view) {
+    p2p_release(*this);
     if (comm) ncclCommDestroy(comm);
     if (ev_packed) cudaEventDestroy(ev_packed);
     if (ev_recvd) cudaEventDestroy(ev_recvd);
@@ -162,6 +163,8 @@ void plan_upload(Plan &pl, cudaStream_t s) {
   const int N = pl.N;
   const size_t o_send = ar.reserve((size_t)pl.send_rows * N * sizeof(float));
   const size_t o_recv = ar.reserve((size_t)pl.recv_rows * N * sizeof(float));
+  // fused-exchange flags: ready[P], consumed[P], err (IPC-exported with the arena)
+  const size_t o_flags = ar.reserve((2 * (size_t)pl.P + 1) * sizeof(int32_t));
   const bool fused = pl.flags & SHIRO_F_FUSED_RECV;
   SpmmLayout l_diag = layout_spmm(ar, pl.A_diag, N);
   SpmmLayout l_out = layout_spmm(ar, pl.A_out, N);
@@ -180,6 +183,9 @@ void plan_upload(Plan &pl, cudaStream_t s) {
   SHIRO_CK(cudaStreamSynchronize(s));
   pl.send_buf = reinterpret_cast<float *>(base + o_send);
   pl.recv_buf = reinterpret_cast<float *>(base + o_recv);
+  pl.xflags = reinterpret_cast<int32_t *>(base + o_flags);
+  pl.recv_buf_off = (int64_t)o_recv;
+  pl.flags_off = (int64_t)o_flags;
   pl.d_diag = bind_spmm(base, l_diag, pl.A_diag, N);
   pl.d_out = bind_spmm(base, l_out, pl.A_out, N);
   pl.d_col = bind_spmm(base, l_col, fused ? empty : pl.A_col, N);
@@ -327,6 +333,57 @@ void exec_flat(Plan &pl, const float *B, float *C, cudaStream_t s) {
   rec(8, s);
   pl.last_launches = launches;
   pl.prof_used = 2;
+}
+
+// Fused exchange (SHIRO_F_XCHG_NCCL unset, P > 1): K4/K3 store rows straight
+// into the peers' receive buffers over NVLink; flags order the producer and
+// consumer sides (p2p.cu).  One stream, no staging copy, no NCCL kernel.
+//   wait CONSUMED >= e-1 (peers done with my previous rows)
+//   K4 pack -> peers, K3 partial SpMM -> peers, signal READY = e at peers
+//   K1 local SpMM (overlaps the NVLink drain of the other ranks)
+//   wait READY >= e from all peers, K2 remote SpMM, K5 scatter-add
+//   signal CONSUMED = e at peers
+void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
+  if (*pl.err_host) throw Error(SHIRO_E_PEER, "fused exchange: a peer did not signal in time");
+  auto rec = [&](int i) {
+    if (pl.prof_on) SHIRO_CK(cudaEventRecord(pl.prof[i], s));
+  };
+  const int P = pl.P;
+  const int32_t e = ++pl.epoch;
+  int32_t *err = pl.xflags + 2 * P;
+  int64_t launches = 0;
+  rec(0);
+  launches += launch_wait(pl.xflags + P, P, e - 1, err, pl.wait_timeout_ns, s);
+  launches += launch_pack_ptr(pl.d_pack.n, pl.d_pack.src, pl.pack_dstp, B, pl.N, s);
+  rec(1);
+  launches += run_spmm(pl.d_out_p2p, B, pl.M, nullptr, nullptr, false, s);
+  rec(2);
+  launches += launch_signal(pl.ready_ptrs, P - 1, e, s);
+  rec(5);
+  launches += stage_local(pl, B, C, s);
+  rec(6);
+  rec(3);
+  launches += launch_wait(pl.xflags, P, e, err, pl.wait_timeout_ns, s);
+  rec(4);
+  if (pl.flags & SHIRO_F_FUSED_RECV) {
+    launches += run_spmm(pl.d_rem, pl.recv_buf, pl.recv_rows, nullptr, C, true, s);
+    rec(7);
+  } else {
+    launches += run_spmm(pl.d_col, pl.recv_buf, pl.recv_rows, nullptr, C, true, s);
+    rec(7);
+    launches += launch_scatter_add(pl.d_scatter.nt, pl.d_scatter.tgt, pl.d_scatter.ptr,
+                                   pl.d_scatter.src, pl.recv_buf, C, pl.N, s);
+  }
+  rec(8);
+  launches += launch_signal(pl.consumed_ptrs, P - 1, e, s);
+  SHIRO_CK(cudaMemcpyAsync(pl.err_host, err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  pl.last_launches = launches;
+  pl.prof_used = 3;
+}
+
+void exec_plan(Plan &pl, const float *B, float *C, cudaStream_t s) {
+  if (pl.p2p) exec_p2p(pl, B, C, s);
+  else exec_flat(pl, B, C, s);
 }
 
 }  // namespace shiro
@@ -559,7 +616,10 @@ int shiro_plan(const shiro_dist_t *d, int64_t n, const int64_t *part, const int6
     plan_phase2(in, p1, in_msgs, pl);
     fill_block_stats(p1, in, pl);
     plan_stats(in, pl, xchg);
-    if (!host_only) plan_upload(pl, s);
+    if (!host_only) {
+      plan_upload(pl, s);
+      if (d->nranks > 1 && !(d->flags & SHIRO_F_XCHG_NCCL)) p2p_setup(pl, xchg);
+    }
     pl.info.plan_seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     *out = h.release();
@@ -672,7 +732,7 @@ int shiro_spmm(shiro_plan_t plan, const float *B_p, float *C_p, void *stream) {
       if (as != ncclSuccess && as != ncclInProgress)
         throw Error(SHIRO_E_NCCL, std::string("asynchronous NCCL error: ") + ncclGetErrorString(as));
     }
-    exec_flat(pl, B_p, C_p, static_cast<cudaStream_t>(stream));
+    exec_plan(pl, B_p, C_p, static_cast<cudaStream_t>(stream));
     SHIRO_CK(cudaGetLastError());
     plan->last_launches = pl.last_launches;
   });
@@ -688,7 +748,7 @@ int shiro_spmm_host(shiro_plan_t plan, const float *B_host, float *C_host, void 
     if (!pl.stage && bytes) SHIRO_CK(cudaMalloc(&pl.stage, 2 * bytes));   // once per plan
     float *dB = pl.stage, *dC = pl.stage ? pl.stage + (size_t)pl.M * pl.N : nullptr;
     if (bytes) SHIRO_CK(cudaMemcpyAsync(dB, B_host, bytes, cudaMemcpyHostToDevice, s));
-    exec_flat(pl, dB, dC, s);
+    exec_plan(pl, dB, dC, s);
     if (bytes) SHIRO_CK(cudaMemcpyAsync(C_host, dC, bytes, cudaMemcpyDeviceToHost, s));
     SHIRO_CK(cudaStreamSynchronize(s));
     plan->last_launches = pl.last_launches;
@@ -802,6 +862,16 @@ int shiro_stage_times(shiro_plan_t plan, double *ms) {
     };
     if (pl.prof_used == 1) {
       ms[SHIRO_STAGE_LOCAL] = ms[SHIRO_STAGE_TOTAL] = el(5, 6);
+      return;
+    }
+    if (pl.prof_used == 3) {   // fused exchange: "exchange" = exposed wait for peers
+      ms[SHIRO_STAGE_PACK] = el(0, 1);
+      ms[SHIRO_STAGE_PARTIAL] = el(1, 2);
+      ms[SHIRO_STAGE_LOCAL] = el(5, 6);
+      ms[SHIRO_STAGE_EXCHANGE] = el(3, 4);
+      ms[SHIRO_STAGE_REMOTE] = el(4, 7);
+      ms[SHIRO_STAGE_SCATTER] = el(7, 8);
+      ms[SHIRO_STAGE_TOTAL] = el(0, 8);
       return;
     }
     ms[SHIRO_STAGE_PACK] = el(0, 1);

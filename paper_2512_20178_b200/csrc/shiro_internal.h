@@ -117,6 +117,18 @@ struct Plan {
   bool prof_on = false;
   cudaEvent_t prof[12] = {};
   int prof_used = 0;
+  // fused NVLink exchange (CUDA IPC peer mappings, p2p_host.cpp)
+  bool p2p = false;
+  int32_t epoch = 0;
+  int32_t *xflags = nullptr;          // local: ready[P], consumed[P], err
+  int64_t recv_buf_off = 0, flags_off = 0;
+  std::vector<void *> peer_base;      // opened IPC mappings
+  void *p2p_arena = nullptr;
+  float *const *pack_dstp = nullptr;
+  int32_t *const *ready_ptrs = nullptr, *const *consumed_ptrs = nullptr;
+  DevSpmm d_out_p2p;
+  int32_t *err_host = nullptr;        // pinned copy of flags[2P]
+  int64_t wait_timeout_ns = 20000000000LL;
   // device staging of B and C for shiro_spmm_host
   float *stage = nullptr;
 
@@ -153,5 +165,10 @@ void plan_upload(Plan &plan, cudaStream_t s);
 
 // executor (runtime.cpp)
 void exec_flat(Plan &plan, const float *B, float *C, cudaStream_t s);
+// fused NVLink exchange (p2p_host.cpp): IPC setup (collective) and executor
+void p2p_setup(Plan &plan, const Alltoallv &xchg);
+void p2p_release(Plan &plan);
+void exec_p2p(Plan &plan, const float *B, float *C, cudaStream_t s);
+void exec_plan(Plan &plan, const float *B, float *C, cudaStream_t s);
 
 }  // namespace shiro

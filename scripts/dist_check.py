@@ -47,7 +47,7 @@ def main():
     flags = 0
     for f in filter(None, args.flags.split(",")):
         flags |= {"fused": sh.F_FUSED_RECV, "colmax": sh.F_COVER_COLMAX, "col": sh.F_MODE_COL,
-                  "row": sh.F_MODE_ROW, "nooverlap": sh.F_NO_OVERLAP}[f]
+                  "row": sh.F_MODE_ROW, "nooverlap": sh.F_NO_OVERLAP, "nccl": sh.F_XCHG_NCCL}[f]
     obj = [sh.get_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     pl = sh.Plan.distributed(rank, world, cfg.n, part, rp_l, col_l, val_l, cfg.N,
@@ -73,11 +73,15 @@ def main():
         lists_ok &= np.array_equal(pl.list(p, sh.LIST_RECV_C), op.send_c.get((p, rank), empty))
     # gather C on rank 0
     sizes = [int(part[r + 1] - part[r]) for r in range(world)]
+    mx = max(sizes)
+    Cpad = torch.zeros((mx, cfg.N), device=dev)      # NCCL gather needs equal sizes
+    Cpad[:hi - lo] = Cd
     if rank == 0:
-        parts = [torch.empty((s, cfg.N), device=dev) for s in sizes]
-        dist.gather(Cd, parts, dst=0)
+        parts = [torch.empty((mx, cfg.N), device=dev) for _ in sizes]
+        dist.gather(Cpad, parts, dst=0)
+        parts = [t[:s] for t, s in zip(parts, sizes)]
     else:
-        dist.gather(Cd, None, dst=0)
+        dist.gather(Cpad, None, dst=0)
     ok_t = torch.tensor([1 if lists_ok else 0], device=dev)
     dist.all_reduce(ok_t, op=dist.ReduceOp.MIN)
     if rank == 0:
