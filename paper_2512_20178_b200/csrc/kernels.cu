@@ -237,8 +237,13 @@ __global__ void __launch_bounds__(kBlock) k_spmm_generic(const SpmmArgs a) {
   const int64_t t = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
   if (t >= a.nrows) return;
   const int64_t kb = a.rp[t], ke = a.rp[t + 1];
-  const int64_t orow = a.out_row ? a.out_row[t] : t;
-  float *y = a.Y + orow * a.N;
+  float *y;
+  if (a.out_ptr) {
+    y = a.out_ptr[t];
+  } else {
+    const int64_t orow = a.out_row ? a.out_row[t] : t;
+    y = a.Y + orow * a.N;
+  }
   for (int c0 = 0; c0 < a.N; c0 += 32 * 4) {
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
     for (int64_t k = kb; k < ke; ++k) {
@@ -426,7 +431,7 @@ int spmm_variant() {
   static int v = -1;
   if (v < 0) {
     const char *e = getenv("SHIRO_KVAR");
-    v = e ? atoi(e) : 0;
+    v = e ? atoi(e) : 4;
   }
   return v;
 }
@@ -436,12 +441,14 @@ void spmm_shape(const SpmmArgs &a, bool acc, cudaStream_t s) {
   if (VPL > 1) { spmm_launch<LPR, VPL, 1, 8>(a, acc, s); return; }
   switch (spmm_variant()) {
     case 1: spmm_launch<LPR, VPL, 3, 8>(a, acc, s); break;
-    case 2: spmm_launch<LPR, VPL, 4, 8>(a, acc, s); break;
     case 3: spmm_launch<LPR, VPL, 4, 4>(a, acc, s); break;
     case 4: spmm_launch<LPR, VPL, 5, 4>(a, acc, s); break;
     case 5: spmm_launch<LPR, VPL, 6, 4>(a, acc, s); break;
-    case 6: spmm_launch<LPR, VPL, 2, 16>(a, acc, s); break;
-    default: spmm_launch<LPR, VPL, 1, 8>(a, acc, s); break;
+    case 6: spmm_launch<LPR, VPL, 1, 8>(a, acc, s); break;
+    case 7: spmm_launch<LPR, VPL, 5, 8>(a, acc, s); break;
+    case 8: spmm_launch<LPR, VPL, 6, 8>(a, acc, s); break;
+    case 2: spmm_launch<LPR, VPL, 4, 8>(a, acc, s); break;
+    default: spmm_launch<LPR, VPL, 5, 4>(a, acc, s); break;   // measured best (c2/c3/c4)
   }
 }
 

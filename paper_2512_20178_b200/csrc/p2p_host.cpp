@@ -135,3 +135,86 @@ void p2p_setup(Plan &pl, const Alltoallv &xchg) {
 }
 
 }  // namespace shiro
+
+namespace shiro {
+
+// ---------------------------------------------------------------------------
+// Hierarchical routing over NVLink: export the route arena (R1 || R2, flags),
+// exchange (handle, offsets of R1/R2/flags, and where the receiver placed
+// each sender's R1 and R2 segments), map the peers, resolve destinations.
+// ---------------------------------------------------------------------------
+namespace {
+struct HierMsg {
+  cudaIpcMemHandle_t handle;
+  int64_t rb_off, flags_off, r1_rows, seg1, seg2;
+};
+}  // namespace
+
+void hier_release(Plan &pl) {
+  Route &R = pl.route;
+  for (void *b : R.peer_base)
+    if (b) cudaIpcCloseMemHandle(b);
+  R.peer_base.clear();
+  if (R.ptrs) cudaFree(R.ptrs);
+  if (R.ops) cudaFree(R.ops);
+  if (R.arena) cudaFree(R.arena);
+  R.ptrs = R.ops = R.arena = nullptr;
+}
+
+void hier_p2p_setup(Plan &pl, const Alltoallv &xchg) {
+  Route &R = pl.route;
+  const int P = pl.P, me = pl.rank;
+  cudaIpcMemHandle_t h;
+  int status = cudaIpcGetMemHandle(&h, R.arena) == cudaSuccess ? 0 : 1;
+  std::vector<std::vector<char>> send(P), recv;
+  for (int d = 0; d < P; ++d) {
+    HierMsg m{h, R.rb_off, R.flags_off, R.r1_rows, R.r1_off[d], R.r2_off[d]};
+    send[d] = bytes_of(m);
+  }
+  xchg(send, recv);
+  R.peer_base.assign(P, nullptr);
+  std::vector<HierMsg> hm(P);
+  for (int d = 0; d < P && status == 0; ++d) {
+    if (d == me) continue;
+    if (recv[d].size() != sizeof(HierMsg)) { status = 1; break; }
+    std::memcpy(&hm[d], recv[d].data(), sizeof(HierMsg));
+    void *base = nullptr;
+    if (cudaIpcOpenMemHandle(&base, hm[d].handle, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      status = 1;
+      break;
+    }
+    R.peer_base[d] = base;
+  }
+  std::vector<std::vector<char>> st_send(P, bytes_of(status)), st_recv;
+  xchg(st_send, st_recv);
+  int any = status;
+  for (int d = 0; d < P; ++d)
+    if (d != me && st_recv[d].size() == sizeof(int)) {
+      int v;
+      std::memcpy(&v, st_recv[d].data(), sizeof(int));
+      any |= v;
+    }
+  if (any) throw Error(SHIRO_E_CUDA, "hierarchical mode needs CUDA IPC peer mappings");
+  const int64_t rowb = (int64_t)pl.N * sizeof(float);
+  hm[me] = HierMsg{h, R.rb_off, R.flags_off, R.r1_rows, R.r1_off[me], R.r2_off[me]};
+  auto seg = [&](int d, int buf) -> char * {
+    char *base = (d == me) ? static_cast<char *>(R.arena) : static_cast<char *>(R.peer_base[d]);
+    const int64_t row = (buf == 0) ? hm[d].seg1 : hm[d].r1_rows + hm[d].seg2;
+    return base + hm[d].rb_off + row * rowb;
+  };
+  auto flag = [&](int d, int i) -> int32_t * {
+    char *base = (d == me) ? static_cast<char *>(R.arena) : static_cast<char *>(R.peer_base[d]);
+    return reinterpret_cast<int32_t *>(base + hm[d].flags_off) + i;
+  };
+  hier_resolve(pl, seg, flag);
+  SHIRO_CK(cudaMallocHost(&pl.err_host, sizeof(int32_t)));
+  *pl.err_host = 0;
+  if (const char *e = getenv("SHIRO_P2P_TIMEOUT_MS")) pl.wait_timeout_ns = atoll(e) * 1000000LL;
+  pl.epoch = 0;
+  std::vector<std::vector<char>> bar_send(P, bytes_of(0)), bar_recv;
+  SHIRO_CK(cudaDeviceSynchronize());
+  xchg(bar_send, bar_recv);
+}
+
+}  // namespace shiro

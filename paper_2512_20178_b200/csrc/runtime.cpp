@@ -24,6 +24,7 @@ namespace shiro {
 Plan::~Plan() {
   if (!loopback_view) {
     p2p_release(*this);
+    hier_release(*this);
     if (comm) ncclCommDestroy(comm);
     if (ev_packed) cudaEventDestroy(ev_packed);
     if (ev_recvd) cudaEventDestroy(ev_recvd);
@@ -61,7 +62,18 @@ size_t put(Arena &ar, const std::vector<T> &v) {
 // nonzeros and kMaxGroupRows rows (2*LPR when an out_row map is used),
 // streamed by one lane group; a per-nonzero byte holds the row offset inside
 // the group.
-constexpr int32_t kChunk = 256;
+// Unit size L: 256 nonzeros for large ops; small ops use smaller units so
+// that they still spread over ~64 lane groups per SM (one lane group walks
+// its unit serially, ~1 memory round trip per U = 8 gathers, so the unit
+// length bounds the latency of small, latency-bound ops).
+constexpr int32_t kChunk = 256, kChunkMin = 32;
+
+int32_t unit_size(int64_t nnz) {
+  if (const char *e = getenv("SHIRO_CHUNK")) return std::max(kChunkMin, atoi(e));
+  int64_t L = nnz / ((int64_t)num_sms() * 64);
+  L = (L / 32) * 32;
+  return (int32_t)std::max<int64_t>(kChunkMin, std::min<int64_t>(kChunk, L));
+}
 constexpr int32_t kMaxGroupRows = 64;
 
 struct SplitHost {
@@ -83,7 +95,7 @@ SplitHost make_split(const HostCsr &c, int N) {
   }
   int lpr, vpl;
   if (!vec_shape(N, &lpr, &vpl)) return s;   // generic path: row per warp
-  s.L = kChunk;
+  s.L = unit_size(c.nnz());
   s.roff.assign(c.nnz(), 0);
   const int64_t max_rows = c.out_row.empty() ? kMaxGroupRows : std::min(kMaxGroupRows, 2 * lpr);
   auto deg = [&](int64_t r) { return c.rp[r + 1] - c.rp[r]; };
@@ -335,6 +347,129 @@ void exec_flat(Plan &pl, const float *B, float *C, cudaStream_t s) {
   pl.prof_used = 2;
 }
 
+// ---------------------------------------------------------------------------
+// Hierarchical routing: device images, destination resolution, executor.
+// ---------------------------------------------------------------------------
+void hier_upload(Plan &pl) {
+  Route &R = pl.route;
+  const int N = pl.N, P = pl.P;
+  Arena ab;
+  const size_t o_rb = ab.reserve((size_t)(R.r1_rows + R.r2_rows) * N * sizeof(float));
+  const size_t o_fl = ab.reserve((3 * (size_t)P + 1) * sizeof(int32_t));
+  SHIRO_CK(cudaMalloc(&R.arena, std::max<size_t>(ab.total, 256)));
+  SHIRO_CK(cudaMemset(R.arena, 0, std::max<size_t>(ab.total, 256)));
+  char *bb = static_cast<char *>(R.arena);
+  R.rb = reinterpret_cast<float *>(bb + o_rb);
+  R.xflags = reinterpret_cast<int32_t *>(bb + o_fl);
+  R.rb_off = (int64_t)o_rb;
+  R.flags_off = (int64_t)o_fl;
+  Arena ar;
+  SpmmLayout lp = layout_spmm(ar, R.s1_part, N);
+  SpmmLayout lg = layout_spmm(ar, R.s2_agg, N);
+  SpmmLayout lf = layout_spmm(ar, R.fin, N);
+  const size_t o_p1 = put(ar, R.s1_pack_src), o_fw = put(ar, R.s2_fwd_src);
+  SHIRO_CK(cudaMalloc(&R.ops, std::max<size_t>(ar.total, 256)));
+  SHIRO_CK(cudaMemset(R.ops, 0, std::max<size_t>(ar.total, 256)));
+  char *base = static_cast<char *>(R.ops);
+  for (const auto &it : ar.items)
+    if (it.src && it.bytes)
+      SHIRO_CK(cudaMemcpy(base + it.off, it.src, it.bytes, cudaMemcpyHostToDevice));
+  R.d_part = bind_spmm(base, lp, R.s1_part, N);
+  R.d_agg = bind_spmm(base, lg, R.s2_agg, N);
+  R.d_fin = bind_spmm(base, lf, R.fin, N);
+  R.d_pack1.n = (int64_t)R.s1_pack_src.size();
+  R.d_pack1.src = reinterpret_cast<const int32_t *>(base + o_p1);
+  R.d_fwd.n = (int64_t)R.s2_fwd_src.size();
+  R.d_fwd.src = reinterpret_cast<const int32_t *>(base + o_fw);
+  pl.info.dev_bytes += (int64_t)(ab.total + ar.total);
+}
+
+void hier_resolve(Plan &pl, const std::function<char *(int, int)> &seg,
+                  const std::function<int32_t *(int, int)> &flag) {
+  Route &R = pl.route;
+  const int P = pl.P, me = pl.rank;
+  const int64_t rowb = (int64_t)pl.N * sizeof(float);
+  std::vector<uint64_t> v;
+  auto add = [&](const std::vector<Dest> &ds) {
+    for (const Dest &d : ds) v.push_back((uint64_t)(seg(d.rank, d.buf) + d.pos * rowb));
+  };
+  add(R.s1_pack_dst);
+  add(R.s1_part_dst);
+  add(R.s2_fwd_dst);
+  add(R.s2_agg_dst);
+  const size_t n_rows = v.size();
+  for (int k = 0; k < 3; ++k)
+    for (int d = 0; d < P; ++d)
+      if (d != me) v.push_back((uint64_t)flag(d, k * P + me));
+  if (R.ptrs) cudaFree(R.ptrs);
+  SHIRO_CK(cudaMalloc(&R.ptrs, std::max<size_t>(8, v.size() * 8)));
+  if (!v.empty()) SHIRO_CK(cudaMemcpy(R.ptrs, v.data(), v.size() * 8, cudaMemcpyHostToDevice));
+  uint64_t *a = static_cast<uint64_t *>(R.ptrs);
+  size_t o = 0;
+  R.pack1_dstp = reinterpret_cast<float *const *>(a + o); o += R.s1_pack_dst.size();
+  R.d_part.a.out_ptr = reinterpret_cast<float *const *>(a + o); o += R.s1_part_dst.size();
+  R.fwd_dstp = reinterpret_cast<float *const *>(a + o); o += R.s2_fwd_dst.size();
+  R.d_agg.a.out_ptr = reinterpret_cast<float *const *>(a + o); o += R.s2_agg_dst.size();
+  if (o != n_rows) throw Error(SHIRO_E_INTERNAL, "route pointer count");
+  R.ready1_ptrs = reinterpret_cast<int32_t *const *>(a + o); o += P - 1;
+  R.ready2_ptrs = reinterpret_cast<int32_t *const *>(a + o); o += P - 1;
+  R.consumed_ptrs = reinterpret_cast<int32_t *const *>(a + o);
+  // own flags never block
+  std::vector<int32_t> f(3 * P + 1, 0);
+  f[me] = f[P + me] = f[2 * P + me] = 0x7fffffff;
+  SHIRO_CK(cudaMemcpy(R.xflags, f.data(), f.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+}
+
+// stage 1: B rows and partial C rows -> R1 (peers and self); stage 2: forward
+// B rows and pre-aggregated partials R1 -> R2 (peers); stage 3: final remote
+// SpMM over [R1 || R2] into C.
+int64_t hier_stage(Plan &pl, int stage, const float *B, float *C, cudaStream_t s) {
+  Route &R = pl.route;
+  int64_t n = 0;
+  if (stage == 1) {
+    n += launch_pack_ptr(R.d_pack1.n, R.d_pack1.src, R.pack1_dstp, B, pl.N, s);
+    n += run_spmm(R.d_part, B, pl.M, nullptr, nullptr, false, s);
+  } else if (stage == 2) {
+    n += launch_pack_ptr(R.d_fwd.n, R.d_fwd.src, R.fwd_dstp, R.rb, pl.N, s);
+    n += run_spmm(R.d_agg, R.rb, R.r1_rows, nullptr, nullptr, false, s);
+  } else {
+    n += run_spmm(R.d_fin, R.rb, R.r1_rows + R.r2_rows, nullptr, C, true, s);
+  }
+  return n;
+}
+
+void exec_hier(Plan &pl, const float *B, float *C, cudaStream_t s) {
+  if (*pl.err_host) throw Error(SHIRO_E_PEER, "hierarchical exchange: a peer did not signal in time");
+  Route &R = pl.route;
+  auto rec = [&](int i) {
+    if (pl.prof_on) SHIRO_CK(cudaEventRecord(pl.prof[i], s));
+  };
+  const int P = pl.P;
+  const int32_t e = ++pl.epoch;
+  int32_t *err = R.xflags + 3 * P;
+  int64_t n = 0;
+  rec(0);
+  n += launch_wait(R.xflags + 2 * P, P, e - 1, err, pl.wait_timeout_ns, s);
+  n += hier_stage(pl, 1, B, C, s);                        // Stage I producers
+  n += launch_signal(R.ready1_ptrs, P - 1, e, s);
+  rec(1);
+  n += stage_local(pl, B, C, s);                          // K1
+  rec(2);
+  n += launch_wait(R.xflags, P, e, err, pl.wait_timeout_ns, s);
+  rec(3);
+  n += hier_stage(pl, 2, B, C, s);                        // Stage II producers
+  n += launch_signal(R.ready2_ptrs, P - 1, e, s);
+  rec(4);
+  n += launch_wait(R.xflags + P, P, e, err, pl.wait_timeout_ns, s);
+  rec(5);
+  n += hier_stage(pl, 3, B, C, s);                        // final remote SpMM
+  rec(6);
+  n += launch_signal(R.consumed_ptrs, P - 1, e, s);
+  SHIRO_CK(cudaMemcpyAsync(pl.err_host, err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  pl.last_launches = n;
+  pl.prof_used = 4;
+}
+
 // Fused exchange (SHIRO_F_XCHG_NCCL unset, P > 1): K4/K3 store rows straight
 // into the peers' receive buffers over NVLink; flags order the producer and
 // consumer sides (p2p.cu).  One stream, no staging copy, no NCCL kernel.
@@ -382,7 +517,8 @@ void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
 }
 
 void exec_plan(Plan &pl, const float *B, float *C, cudaStream_t s) {
-  if (pl.p2p) exec_p2p(pl, B, C, s);
+  if (pl.route.active && pl.P > 1) exec_hier(pl, B, C, s);
+  else if (pl.p2p) exec_p2p(pl, B, C, s);
   else exec_flat(pl, B, C, s);
 }
 
@@ -614,11 +750,25 @@ int shiro_plan(const shiro_dist_t *d, int64_t n, const int64_t *part, const int6
     xchg(p1.out, in_msgs);
     in_msgs.resize(d->nranks);
     plan_phase2(in, p1, in_msgs, pl);
+    const bool hier = d->group_size > 1 && d->nranks > 1;
+    if (hier) {
+      if (d->flags & SHIRO_F_XCHG_NCCL)
+        throw Error(SHIRO_E_ARG, "the hierarchical schedule uses the fused NVLink exchange");
+      std::vector<std::vector<char>> meta;
+      xchg(hier_meta_messages(pl), meta);
+      meta.resize(d->nranks);
+      hier_build(in, p1, pl, meta);
+    }
     fill_block_stats(p1, in, pl);
     plan_stats(in, pl, xchg);
     if (!host_only) {
       plan_upload(pl, s);
-      if (d->nranks > 1 && !(d->flags & SHIRO_F_XCHG_NCCL)) p2p_setup(pl, xchg);
+      if (hier) {
+        hier_upload(pl);
+        hier_p2p_setup(pl, xchg);
+      } else if (d->nranks > 1 && !(d->flags & SHIRO_F_XCHG_NCCL)) {
+        p2p_setup(pl, xchg);
+      }
     }
     pl.info.plan_seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -669,6 +819,16 @@ int shiro_plan_loopback(int32_t nranks, int32_t group_size, uint32_t flags, int6
       plan_phase2(ins[r], p1[r], inbox[r], pl);
       fill_block_stats(p1[r], ins[r], pl);
     }
+    const bool hier = group_size > 1 && P > 1;
+    if (hier) {
+      std::vector<std::vector<std::vector<char>>> mbox(P, std::vector<std::vector<char>>(P));
+      for (int r = 0; r < P; ++r) {
+        auto out_m = hier_meta_messages(*h->ranks[r]);
+        for (int q = 0; q < P; ++q)
+          if (q != r) mbox[q][r] = std::move(out_m[q]);
+      }
+      for (int r = 0; r < P; ++r) hier_build(ins[r], p1[r], *h->ranks[r], mbox[r]);
+    }
     // stats exchange among virtual ranks: run plan_stats sequentially with a
     // transport that serves precomputed vectors (two passes)
     std::vector<std::vector<char>> shares(P);
@@ -693,9 +853,23 @@ int shiro_plan_loopback(int32_t nranks, int32_t group_size, uint32_t flags, int6
       Plan &pl = *h->ranks[r];
       if (!host_only) {
         plan_upload(pl, s);
+        if (hier) hier_upload(pl);
       }
       pl.info.plan_seconds =
           std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+    if (hier && !host_only) {
+      // same-device "peers": destinations are the other virtual ranks' buffers
+      for (int r = 0; r < P; ++r) {
+        Plan &pl = *h->ranks[r];
+        auto seg = [&, r](int d, int buf) -> char * {
+          Route &D = h->ranks[d]->route;
+          const int64_t row = (buf == 0) ? D.r1_off[r] : D.r1_rows + D.r2_off[r];
+          return reinterpret_cast<char *>(D.rb) + row * (int64_t)pl.N * (int64_t)sizeof(float);
+        };
+        auto flag = [&](int d, int i) -> int32_t * { return h->ranks[d]->route.xflags + i; };
+        hier_resolve(pl, seg, flag);
+      }
     }
     *out = h.release();
   });
@@ -768,6 +942,11 @@ int shiro_spmm_loopback(shiro_plan_t plan, const float *B, float *C, void *strea
     auto Cp = [&](int r) { return C + plan->ranks[r]->part[r] * N; };
     if (P == 1) {
       launches += stage_local(*plan->ranks[0], Bp(0), Cp(0), s);
+    } else if (plan->ranks[0]->route.active) {
+      for (int r = 0; r < P; ++r) launches += hier_stage(*plan->ranks[r], 1, Bp(r), Cp(r), s);
+      for (int r = 0; r < P; ++r) launches += stage_local(*plan->ranks[r], Bp(r), Cp(r), s);
+      for (int r = 0; r < P; ++r) launches += hier_stage(*plan->ranks[r], 2, Bp(r), Cp(r), s);
+      for (int r = 0; r < P; ++r) launches += hier_stage(*plan->ranks[r], 3, Bp(r), Cp(r), s);
     } else {
       for (int r = 0; r < P; ++r) launches += stage_send(*plan->ranks[r], Bp(r), s);
       // exchange: device copies send(s -> r) into recv(r from s)
@@ -830,6 +1009,14 @@ int shiro_plan_list(shiro_plan_t plan, int32_t peer, int32_t kind, int64_t *buf,
       case SHIRO_LIST_SEND_C: v = &pl.send_c[peer]; break;
       case SHIRO_LIST_RECV_B: v = &pl.recv_b[peer]; break;
       case SHIRO_LIST_RECV_C: v = &pl.recv_c[peer]; break;
+      case SHIRO_LIST_H1_SEND: case SHIRO_LIST_H2_SEND:
+      case SHIRO_LIST_H1_RECV: case SHIRO_LIST_H2_RECV: {
+        if (!pl.route.active) throw Error(SHIRO_E_ARG, "not a hierarchical plan");
+        const int st = (kind == SHIRO_LIST_H1_SEND || kind == SHIRO_LIST_H1_RECV) ? 0 : 1;
+        const bool snd = kind == SHIRO_LIST_H1_SEND || kind == SHIRO_LIST_H2_SEND;
+        v = snd ? &pl.route.h_send[st][peer] : &pl.route.h_recv[st][peer];
+        break;
+      }
       default: throw Error(SHIRO_E_ARG, "unknown list kind");
     }
     *len = (int64_t)v->size();
@@ -862,6 +1049,15 @@ int shiro_stage_times(shiro_plan_t plan, double *ms) {
     };
     if (pl.prof_used == 1) {
       ms[SHIRO_STAGE_LOCAL] = ms[SHIRO_STAGE_TOTAL] = el(5, 6);
+      return;
+    }
+    if (pl.prof_used == 4) {   // hierarchical: PACK = Stage I, PARTIAL = Stage II producers
+      ms[SHIRO_STAGE_PACK] = el(0, 1);
+      ms[SHIRO_STAGE_LOCAL] = el(1, 2);
+      ms[SHIRO_STAGE_EXCHANGE] = el(2, 3) + el(4, 5);
+      ms[SHIRO_STAGE_PARTIAL] = el(3, 4);
+      ms[SHIRO_STAGE_REMOTE] = el(5, 6);
+      ms[SHIRO_STAGE_TOTAL] = el(0, 6);
       return;
     }
     if (pl.prof_used == 3) {   // fused exchange: "exchange" = exposed wait for peers

@@ -69,6 +69,46 @@ struct DevScatter {
   int64_t nsrc = 0;
 };
 
+// Destination of a produced row in the hierarchical routing: the segment of
+// the sending rank inside buffer `buf` (0 = R1, 1 = R2) of rank `rank`.
+struct Dest {
+  int32_t rank, buf;
+  int64_t pos;
+};
+
+// Hierarchical (two-stage) routing of one rank (hier.cpp).
+struct Route {
+  bool active = false;
+  int64_t r1_rows = 0, r2_rows = 0;
+  std::vector<int64_t> r1_off, r2_off;                 // segment offset per source (rows)
+  std::vector<std::vector<int64_t>> h_send[2], h_recv[2];
+  // Stage I producers (read B_local)
+  std::vector<int32_t> s1_pack_src;
+  std::vector<Dest> s1_pack_dst;
+  HostCsr s1_part;
+  std::vector<Dest> s1_part_dst;
+  // Stage II producers (read own R1)
+  std::vector<int32_t> s2_fwd_src;
+  std::vector<Dest> s2_fwd_dst;
+  HostCsr s2_agg;
+  std::vector<Dest> s2_agg_dst;
+  // final remote SpMM over [R1 || R2]
+  HostCsr fin;
+  // device state
+  void *arena = nullptr;           // R1 || R2 and flags (IPC-exported)
+  float *rb = nullptr;
+  int32_t *xflags = nullptr;       // ready1[P], ready2[P], consumed[P], err
+  int64_t rb_off = 0, flags_off = 0;
+  void *ops = nullptr;             // op arrays
+  void *ptrs = nullptr;            // resolved destination pointers
+  DevSpmm d_part, d_agg, d_fin;
+  DevPack d_pack1, d_fwd;
+  float *const *pack1_dstp = nullptr, *const *fwd_dstp = nullptr;
+  int32_t *const *ready1_ptrs = nullptr, *const *ready2_ptrs = nullptr,
+          *const *consumed_ptrs = nullptr;
+  std::vector<void *> peer_base;   // opened IPC mappings
+};
+
 // Plan-time transport: collective all-to-allv of host byte segments.
 using Alltoallv = std::function<void(const std::vector<std::vector<char>> &send,
                                      std::vector<std::vector<char>> &recv)>;
@@ -89,8 +129,8 @@ struct Plan {
   std::vector<int64_t> send_off, recv_off;   // rows, [P+1]
   int64_t send_rows = 0, recv_rows = 0;
 
-  // hierarchical stage lists (group_size > 1): per stage, per peer
-  std::vector<std::vector<int64_t>> h_send[2], h_recv[2];
+  // hierarchical routing (group_size > 1)
+  Route route;
 
   // host images of the ops
   HostCsr A_diag, A_out, A_col, A_rem;
@@ -162,6 +202,20 @@ void plan_phase2(const PlanInput &in, Phase1 &p1, const std::vector<std::vector<
 void plan_stats(const PlanInput &in, Plan &plan, const Alltoallv &xchg);
 // device upload
 void plan_upload(Plan &plan, cudaStream_t s);
+
+// hierarchical routing (hier.cpp, runtime.cpp, p2p_host.cpp)
+std::vector<std::vector<char>> hier_meta_messages(const Plan &pl);
+void hier_build(const PlanInput &in, const Phase1 &p1, Plan &pl,
+                const std::vector<std::vector<char>> &meta);
+void hier_upload(Plan &pl);
+// resolve destinations: seg(d, buf) = address of THIS rank's segment in
+// buffer buf of rank d; flag(d, i) = address of flag i of rank d
+void hier_resolve(Plan &pl, const std::function<char *(int, int)> &seg,
+                  const std::function<int32_t *(int, int)> &flag);
+void hier_p2p_setup(Plan &pl, const Alltoallv &xchg);
+void hier_release(Plan &pl);
+void exec_hier(Plan &pl, const float *B, float *C, cudaStream_t s);
+int64_t hier_stage(Plan &pl, int stage, const float *B, float *C, cudaStream_t s);
 
 // executor (runtime.cpp)
 void exec_flat(Plan &plan, const float *B, float *C, cudaStream_t s);

@@ -1,6 +1,4 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-rm -f gpurun_out/sweep.txt
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1
-bash scripts/sweep.sh "c2 c4 c3" "SHIRO_KVAR=0;SHIRO_KVAR=1;SHIRO_KVAR=2;SHIRO_KVAR=3;SHIRO_KVAR=4;SHIRO_KVAR=5;SHIRO_KVAR=6"
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1
 echo done

@@ -123,3 +123,59 @@ def test_invalid_inputs_rejected():
         sh.Plan.loopback(2, n, part, *good, 0, flags=sh.F_HOST_ONLY)
     with pytest.raises(sh.ShiroError, match="SHIRO_E_ARG"):          # g must divide P
         sh.Plan.loopback(2, n, part, *good, 4, group_size=3, flags=sh.F_HOST_ONLY)
+
+
+def oracle_hier_lists(msgs, P):
+    """Per (stage, src, dst): B-row ids (owners ascending) then C-row ids grouped
+    by final destination ascending -- the SHIRO_LIST_H*_ format."""
+    out = {}
+    for st in (1, 2):
+        for s in range(P):
+            for d in range(P):
+                ms = [m for m in msgs if m.stage == st and m.src == s and m.dst == d]
+                b = [m for m in ms if m.kind == "B"]
+                c = [m for m in ms if m.kind in ("C", "CA")]
+                b.sort(key=lambda m: m.owner if m.owner >= 0 else s)
+                c.sort(key=lambda m: m.final)
+                ids = [x for m in b for x in m.ids.tolist()] + [x for m in c for x in m.ids.tolist()]
+                out[(st, s, d)] = np.array(ids, np.int64)
+    return out
+
+
+@pytest.mark.parametrize("P,g,seed", [(4, 2, 0), (8, 2, 1), (8, 4, 2), (8, 4, 3), (6, 3, 4), (8, 8, 5)])
+def test_hier_lists_bit_exact(P, g, seed):
+    rng = np.random.default_rng(500 + seed)
+    n = int(rng.integers(80, 400))
+    row_ptr, col, val = random_csr(rng, n, float(rng.uniform(0.01, 0.08)), symmetric=seed % 2 == 0)
+    part = oracle.uniform_partition(n, P)
+    pl = sh.Plan.loopback(P, n, part, row_ptr, col, val, 8, group_size=g, flags=sh.F_HOST_ONLY)
+    op = oracle.plan_flat(n, part, row_ptr, col)
+    ref = oracle_hier_lists(oracle.plan_hier(op, g), P)
+    for r in range(P):
+        v = pl.rank_view(r)
+        for p in range(P):
+            if p == r:
+                continue
+            for st, ks, kr in ((1, sh.LIST_H1_SEND, sh.LIST_H1_RECV), (2, sh.LIST_H2_SEND, sh.LIST_H2_RECV)):
+                assert np.array_equal(v.list(p, ks), ref[(st, r, p)]), (st, r, p)
+                assert np.array_equal(v.list(p, kr), ref[(st, p, r)]), (st, p, r)
+
+
+@pytest.mark.parametrize("name", ["hier_col.txt", "hier_row.txt"])
+def test_hier_fixture_lists(name):
+    from conftest import csr_from_entries, load_golden
+    meta, entries, ex = load_golden(name)
+    n, P, g = meta["n"], meta["P"], meta["g"]
+    row_ptr, col, val = csr_from_entries(n, entries)
+    part = oracle.uniform_partition(n, P)
+    pl = sh.Plan.loopback(P, n, part, row_ptr, col, val, 4, group_size=g, flags=sh.F_HOST_ONLY)
+    info = pl.info()
+    assert info["g_hier_inter_rows"] == ex["hier_inter_rows"] == 4
+    assert info["g_flat_inter_rows"] == ex["flat_inter_rows"] == 8
+    inter = 0
+    for r in range(P):
+        v = pl.rank_view(r)
+        for p in range(P):
+            if p != r and p // g != r // g:
+                inter += v.list(p, sh.LIST_H1_SEND).size + v.list(p, sh.LIST_H2_SEND).size
+    assert inter == 4                                     # 8 -> 4 (PAPER.md L517, L519)
