@@ -245,7 +245,7 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--group-size", type=int, default=1)
-    ap.add_argument("--fused", action="store_true", help="SHIRO_F_FUSED_RECV")
+    ap.add_argument("--split-recv", action="store_true", help="SHIRO_F_SPLIT_RECV (K2 and K5 as two launches)")
     ap.add_argument("--colmax", action="store_true", help="SHIRO_F_COVER_COLMAX")
     ap.add_argument("--mode", default="joint", choices=["joint", "col", "row"])
     ap.add_argument("--xchg", default="p2p", choices=["p2p", "nccl"],
@@ -288,8 +288,8 @@ def main():
     B_p = shiro_gen.gen_B(cfg.seed, lo, M, cfg.N)
 
     flags = 0
-    if args.fused:
-        flags |= sh.F_FUSED_RECV
+    if args.split_recv:
+        flags |= sh.F_SPLIT_RECV
     if args.colmax:
         flags |= sh.F_COVER_COLMAX
     flags |= {"joint": 0, "col": sh.F_MODE_COL, "row": sh.F_MODE_ROW}[args.mode]
@@ -430,7 +430,7 @@ def main():
             "data": "synthetic",
             "config": {"workload": f"{cfg.name}: {cfg.desc}", "n": cfg.n, "nnz": nnz, "N": cfg.N,
                        "P": world, "group_size": args.group_size,
-                       "plan": ("fused-recv " if args.fused else "") + args.mode +
+                       "plan": ("split-recv " if args.split_recv else "") + args.mode +
                                (" col-max" if args.colmax else " row-max"),
                        "partition": "uniform 1D rows (larger blocks first)",
                        "l2": "flushed (256 MiB memset) before every timed step",

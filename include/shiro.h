@@ -64,7 +64,8 @@ enum shiro_status {
 #define SHIRO_F_MODE_JOINT 0u          /* joint row/column   */
 #define SHIRO_F_MODE_COL (1u << 1)     /* column-based only (Eq. 2)    */
 #define SHIRO_F_MODE_ROW (1u << 2)     /* row-based only (Eq. 3)       */
-#define SHIRO_F_FUSED_RECV (1u << 3)   /* remote SpMM + scatter-add in one pass  */
+#define SHIRO_F_SPLIT_RECV (1u << 3)   /* remote SpMM (K2) and scatter-add (K5) as
+                                          two launches; default: one fused pass  */
 #define SHIRO_F_HOST_ONLY (1u << 4)    /* plan lists/stats only, no device state */
 #define SHIRO_F_NO_OVERLAP (1u << 5)   /* local SpMM after the exchange (ablation)*/
 #define SHIRO_F_XCHG_NCCL (1u << 6)    /* exchange with NCCL grouped send/recv

@@ -54,6 +54,14 @@ __device__ __forceinline__ void add4(float4 &acc, const float4 &x) {
   acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
 }
 
+// Output row address of a pointer-routed row: a peer (or own) buffer address,
+// or -- top bit set -- a row index into Y (the caller's C: local rows of the
+// fused producer launch, whose address is only known at call time).
+__device__ __forceinline__ float4 *out_addr(const SpmmArgs &a, long long v) {
+  if (v < 0) return reinterpret_cast<float4 *>(a.Y + (v & 0x7fffffffffffffffLL) * a.N);
+  return reinterpret_cast<float4 *>(v);
+}
+
 // Source row in the unified row space [X0 || X1] (X1 unused when n0 covers all).
 template <bool TWO>
 __device__ __forceinline__ const float4 *src_row(const SpmmArgs &a, int c) {
@@ -99,8 +107,9 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
     const int64_t t = a.long_row[lr];
     const int f = a.long_first[lr], nch = a.long_first[lr + 1] - f;
     const int64_t rb = __ldg(a.rp + t), re = __ldg(a.rp + t + 1);
-    const int64_t kb = rb + (int64_t)(u - f) * a.L;
-    const int64_t ke = (kb + a.L < re) ? kb + a.L : re;
+    const int64_t clen = (re - rb + nch - 1) / nch;     // chunk length of this hub row
+    const int64_t kb = rb + (int64_t)(u - f) * clen;
+    const int64_t ke = (kb + clen < re) ? kb + clen : re;
     for (int64_t base = kb; base < ke; base += LPR) {
       const int64_t k = base + li;
       int2 cv = make_int2(0, 0);
@@ -129,14 +138,24 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
       float4 s[VPL];
 #pragma unroll
       for (int q = 0; q < VPL; ++q) s[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int c = 0; c < nch; ++c) {        // fixed chunk order: deterministic
-        const float4 *cp = reinterpret_cast<const float4 *>(a.scratch + (int64_t)(f + c) * a.N);
+      // fixed chunk order (deterministic); 8 partial loads in flight
+      for (int c0 = 0; c0 < nch; c0 += 8) {
+        float4 pv[8][VPL];
 #pragma unroll
-        for (int q = 0; q < VPL; ++q) add4(s[q], __ldcg(cp + li + q * LPR));
+        for (int c = 0; c < 8; ++c) {
+          const float4 *cp = reinterpret_cast<const float4 *>(a.scratch + (int64_t)(f + c0 + c) * a.N);
+#pragma unroll
+          for (int q = 0; q < VPL; ++q)
+            pv[c][q] = (c0 + c < nch) ? __ldcg(cp + li + q * LPR) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+#pragma unroll
+          for (int q = 0; q < VPL; ++q) add4(s[q], pv[c][q]);
       }
       float4 *y;
       if (OUTP) {
-        y = reinterpret_cast<float4 *>(a.out_ptr[t]);
+        y = out_addr(a, (long long)a.out_ptr[t]);
       } else {
         const int64_t orow = a.out_row ? a.out_row[t] : t;
         y = reinterpret_cast<float4 *>(a.Y + orow * a.N);
@@ -172,7 +191,7 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
     float4 *y;
     if (OUTP) {
       const long long sel = (cur < LPR) ? opw0 : opw1;
-      y = reinterpret_cast<float4 *>(__shfl_sync(mask, sel, cur & (LPR - 1), LPR));
+      y = out_addr(a, __shfl_sync(mask, sel, cur & (LPR - 1), LPR));
     } else {
       int64_t orow;
       if (a.out_row) {
@@ -239,7 +258,8 @@ __global__ void __launch_bounds__(kBlock) k_spmm_generic(const SpmmArgs a) {
   const int64_t kb = a.rp[t], ke = a.rp[t + 1];
   float *y;
   if (a.out_ptr) {
-    y = a.out_ptr[t];
+    const long long v = (long long)a.out_ptr[t];
+    y = (v < 0) ? a.Y + (v & 0x7fffffffffffffffLL) * a.N : reinterpret_cast<float *>(v);
   } else {
     const int64_t orow = a.out_row ? a.out_row[t] : t;
     y = a.Y + orow * a.N;

@@ -38,6 +38,8 @@ void p2p_release(Plan &pl) {
   pl.peer_base.clear();
   if (pl.p2p_arena) cudaFree(pl.p2p_arena);
   pl.p2p_arena = nullptr;
+  if (pl.prod_ops) cudaFree(pl.prod_ops);
+  pl.prod_ops = nullptr;
   if (pl.err_host) cudaFreeHost(pl.err_host);
   pl.err_host = nullptr;
   pl.p2p = false;
@@ -103,21 +105,17 @@ void p2p_setup(Plan &pl, const Alltoallv &xchg) {
   }
   if ((int64_t)outp.size() != pl.d_out.a.nrows || (int64_t)dstp.size() != pl.d_pack.n)
     throw Error(SHIRO_E_INTERNAL, "fused exchange: row count mismatch");
-  const size_t n_all = dstp.size() + outp.size() + rdy.size() + cons.size();
+  upload_prod(pl, dstp, outp);          // K4 + K3 + K1 as one pointer-routed launch
+  const size_t n_all = rdy.size() + cons.size();
   SHIRO_CK(cudaMalloc(&pl.p2p_arena, std::max<size_t>(8, n_all * sizeof(uint64_t))));
   uint64_t *a = static_cast<uint64_t *>(pl.p2p_arena);
   std::vector<uint64_t> all;
-  all.insert(all.end(), dstp.begin(), dstp.end());
-  all.insert(all.end(), outp.begin(), outp.end());
   all.insert(all.end(), rdy.begin(), rdy.end());
   all.insert(all.end(), cons.begin(), cons.end());
   if (!all.empty())
     SHIRO_CK(cudaMemcpy(a, all.data(), all.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
-  pl.pack_dstp = reinterpret_cast<float *const *>(a);
-  pl.d_out_p2p = pl.d_out;
-  pl.d_out_p2p.a.out_ptr = reinterpret_cast<float *const *>(a + dstp.size());
-  pl.ready_ptrs = reinterpret_cast<int32_t *const *>(a + dstp.size() + outp.size());
-  pl.consumed_ptrs = reinterpret_cast<int32_t *const *>(a + dstp.size() + outp.size() + rdy.size());
+  pl.ready_ptrs = reinterpret_cast<int32_t *const *>(a);
+  pl.consumed_ptrs = reinterpret_cast<int32_t *const *>(a + rdy.size());
   // 5. local flags: own entries never block (INT_MAX), the rest start at 0
   std::vector<int32_t> f(2 * P + 1, 0);
   f[me] = INT_MAX;

@@ -10,9 +10,10 @@
 //   s0: K1 C = A_diag * B               (E4, overlapped with E3)
 //   s0: wait ev_recvd
 //   s0: K2 C += A_col * recv_B          (E5)
-//   s0: K5 C += sum of recv partials     (E6)   [or K2+K5 fused: FUSED_RECV]
+//   s0: K5 C += sum of recv partials     (E6)   [default: K2+K5 in one pass; SHIRO_F_SPLIT_RECV: two launches]
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -97,14 +98,18 @@ SplitHost make_split(const HostCsr &c, int N) {
   if (!vec_shape(N, &lpr, &vpl)) return s;   // generic path: row per warp
   s.L = unit_size(c.nnz());
   s.roff.assign(c.nnz(), 0);
-  const int64_t max_rows = c.out_row.empty() ? kMaxGroupRows : std::min(kMaxGroupRows, 2 * lpr);
+  const int64_t max_rows = (c.out_row.empty() && !c.ptr_rows) ? kMaxGroupRows
+                                                              : std::min(kMaxGroupRows, 2 * lpr);
   auto deg = [&](int64_t r) { return c.rp[r + 1] - c.rp[r]; };
   int64_t t = 0;
   while (t < c.nrows) {
     if (deg(t) > s.L) {
       const int32_t lr = (int32_t)s.long_row.size();
       s.long_row.push_back((int32_t)t);
-      const int64_t nch = (deg(t) + s.L - 1) / s.L;
+      // chunk length ~max(L, sqrt(deg)): balances the serial walk of one chunk
+      // against the in-order reduction of the chunk partials (both ~latency-bound)
+      const int64_t clen = std::max<int64_t>(s.L, (int64_t)std::sqrt((double)deg(t)));
+      const int64_t nch = (deg(t) + clen - 1) / clen;
       for (int64_t k = 0; k < nch; ++k) s.task_long.push_back(lr);
       s.long_first.push_back((int32_t)s.task_long.size());
       ++t;
@@ -177,7 +182,7 @@ void plan_upload(Plan &pl, cudaStream_t s) {
   const size_t o_recv = ar.reserve((size_t)pl.recv_rows * N * sizeof(float));
   // fused-exchange flags: ready[P], consumed[P], err (IPC-exported with the arena)
   const size_t o_flags = ar.reserve((2 * (size_t)pl.P + 1) * sizeof(int32_t));
-  const bool fused = pl.flags & SHIRO_F_FUSED_RECV;
+  const bool fused = !(pl.flags & SHIRO_F_SPLIT_RECV);
   SpmmLayout l_diag = layout_spmm(ar, pl.A_diag, N);
   SpmmLayout l_out = layout_spmm(ar, pl.A_out, N);
   HostCsr empty;
@@ -237,13 +242,74 @@ void plan_upload(Plan &pl, cudaStream_t s) {
     SHIRO_CK(cudaEventCreateWithFlags(&pl.ev_packed, cudaEventDisableTiming));
     SHIRO_CK(cudaEventCreateWithFlags(&pl.ev_recvd, cudaEventDisableTiming));
   }
-  // host images are no longer needed
+}
+
+// Host images are dropped once every device image has been built.
+void plan_drop_host(Plan &pl) {
   pl.A_diag = HostCsr(); pl.A_out = HostCsr(); pl.A_col = HostCsr(); pl.A_rem = HostCsr();
   std::vector<int32_t>().swap(pl.pack_src);
   std::vector<int32_t>().swap(pl.pack_dst);
   std::vector<int32_t>().swap(pl.sc_tgt);
   std::vector<int32_t>().swap(pl.sc_src);
   std::vector<int64_t>(1, 0).swap(pl.sc_ptr);
+  pl.route.s1_part = HostCsr(); pl.route.s2_agg = HostCsr(); pl.route.fin = HostCsr();
+}
+
+// Fused producer op of the fused exchange: one SpMM launch whose rows are
+// (1) the packed B rows (one unit-weight nonzero each, K4), (2) the
+// row-based partial rows (A_out, K3) -- both stored at peer addresses -- and
+// (3) the local rows (A_diag, K1) stored into C (tagged row index).  Peer rows
+// come first so their NVLink stores start early.
+void upload_prod(Plan &pl, const std::vector<uint64_t> &pack_addr,
+                 const std::vector<uint64_t> &part_addr) {
+  HostCsr c;
+  c.ptr_rows = true;
+  std::vector<uint64_t> outp;
+  const int64_t np = (int64_t)pl.pack_src.size();
+  for (int64_t i = 0; i < np; ++i) {
+    c.col.push_back(pl.pack_src[i]);
+    c.val.push_back(1.0f);
+    c.rp.push_back((int64_t)c.col.size());
+    outp.push_back(pack_addr[i]);
+  }
+  for (int64_t t = 0; t < pl.A_out.nrows; ++t) {
+    for (int64_t k = pl.A_out.rp[t]; k < pl.A_out.rp[t + 1]; ++k) {
+      c.col.push_back(pl.A_out.col[k]);
+      c.val.push_back(pl.A_out.val[k]);
+    }
+    c.rp.push_back((int64_t)c.col.size());
+    outp.push_back(part_addr[t]);
+  }
+  for (int64_t t = 0; t < pl.A_diag.nrows; ++t) {
+    for (int64_t k = pl.A_diag.rp[t]; k < pl.A_diag.rp[t + 1]; ++k) {
+      c.col.push_back(pl.A_diag.col[k]);
+      c.val.push_back(pl.A_diag.val[k]);
+    }
+    c.rp.push_back((int64_t)c.col.size());
+    outp.push_back((1ull << 63) | (uint64_t)t);       // local row of C
+  }
+  c.nrows = (int64_t)outp.size();
+  Arena ar;
+  SpmmLayout L = layout_spmm(ar, c, pl.N);
+  const size_t o_ptr = put(ar, outp);
+  SHIRO_CK(cudaMalloc(&pl.prod_ops, std::max<size_t>(ar.total, 256)));
+  SHIRO_CK(cudaMemset(pl.prod_ops, 0, std::max<size_t>(ar.total, 256)));
+  char *base = static_cast<char *>(pl.prod_ops);
+  for (const auto &it : ar.items)
+    if (it.src && it.bytes)
+      SHIRO_CK(cudaMemcpy(base + it.off, it.src, it.bytes, cudaMemcpyHostToDevice));
+  pl.d_prod = bind_spmm(base, L, c, pl.N);
+  pl.d_prod.a.out_ptr = reinterpret_cast<float *const *>(base + o_ptr);
+  pl.info.dev_bytes += (int64_t)ar.total;
+  // the fused launch is the "local" op of a step; pack/partial fold into it
+  std::vector<int32_t> src(c.col);
+  std::sort(src.begin(), src.end());
+  pl.info.op_nnz[SHIRO_OP_LOCAL] = c.nnz();
+  pl.info.op_rows[SHIRO_OP_LOCAL] = c.nrows;
+  pl.info.op_src_rows[SHIRO_OP_LOCAL] = (int64_t)(std::unique(src.begin(), src.end()) - src.begin());
+  pl.info.op_nnz[SHIRO_OP_PACK] = pl.info.op_rows[SHIRO_OP_PACK] = pl.info.op_src_rows[SHIRO_OP_PACK] = 0;
+  pl.info.op_nnz[SHIRO_OP_PARTIAL] = pl.info.op_rows[SHIRO_OP_PARTIAL] = 0;
+  pl.info.op_src_rows[SHIRO_OP_PARTIAL] = 0;
 }
 
 namespace {
@@ -267,7 +333,7 @@ int64_t stage_send(Plan &pl, const float *B, cudaStream_t s) {
 // E5 + E6: consume the receive buffer
 int64_t stage_recv(Plan &pl, float *C, cudaStream_t s) {
   int64_t n = 0;
-  if (pl.flags & SHIRO_F_FUSED_RECV) {
+  if (!(pl.flags & SHIRO_F_SPLIT_RECV)) {
     n += run_spmm(pl.d_rem, pl.recv_buf, pl.recv_rows, nullptr, C, true, s);
   } else {
     n += run_spmm(pl.d_col, pl.recv_buf, pl.recv_rows, nullptr, C, true, s);
@@ -333,7 +399,7 @@ void exec_flat(Plan &pl, const float *B, float *C, cudaStream_t s) {
     launches += stage_local(pl, B, C, s);
     rec(6, s);
   }
-  if (pl.flags & SHIRO_F_FUSED_RECV) {
+  if (!(pl.flags & SHIRO_F_SPLIT_RECV)) {
     launches += run_spmm(pl.d_rem, pl.recv_buf, pl.recv_rows, nullptr, C, true, s);
     rec(7, s);
   } else {
@@ -474,10 +540,10 @@ void exec_hier(Plan &pl, const float *B, float *C, cudaStream_t s) {
 // into the peers' receive buffers over NVLink; flags order the producer and
 // consumer sides (p2p.cu).  One stream, no staging copy, no NCCL kernel.
 //   wait CONSUMED >= e-1 (peers done with my previous rows)
-//   K4 pack -> peers, K3 partial SpMM -> peers, signal READY = e at peers
-//   K1 local SpMM (overlaps the NVLink drain of the other ranks)
-//   wait READY >= e from all peers, K2 remote SpMM, K5 scatter-add
-//   signal CONSUMED = e at peers
+//   one launch: K4 pack + K3 partial SpMM -> peers' buffers, K1 local -> C
+//   signal READY = e at peers
+//   wait READY >= e from all peers, K2 remote SpMM + K5 scatter-add (fused
+//   by default), signal CONSUMED = e at peers
 void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
   if (*pl.err_host) throw Error(SHIRO_E_PEER, "fused exchange: a peer did not signal in time");
   auto rec = [&](int i) {
@@ -489,18 +555,16 @@ void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
   int64_t launches = 0;
   rec(0);
   launches += launch_wait(pl.xflags + P, P, e - 1, err, pl.wait_timeout_ns, s);
-  launches += launch_pack_ptr(pl.d_pack.n, pl.d_pack.src, pl.pack_dstp, B, pl.N, s);
   rec(1);
-  launches += run_spmm(pl.d_out_p2p, B, pl.M, nullptr, nullptr, false, s);
   rec(2);
-  launches += launch_signal(pl.ready_ptrs, P - 1, e, s);
   rec(5);
-  launches += stage_local(pl, B, C, s);
+  launches += run_spmm(pl.d_prod, B, pl.M, nullptr, C, false, s);
   rec(6);
+  launches += launch_signal(pl.ready_ptrs, P - 1, e, s);
   rec(3);
   launches += launch_wait(pl.xflags, P, e, err, pl.wait_timeout_ns, s);
   rec(4);
-  if (pl.flags & SHIRO_F_FUSED_RECV) {
+  if (!(pl.flags & SHIRO_F_SPLIT_RECV)) {
     launches += run_spmm(pl.d_rem, pl.recv_buf, pl.recv_rows, nullptr, C, true, s);
     rec(7);
   } else {
@@ -769,6 +833,7 @@ int shiro_plan(const shiro_dist_t *d, int64_t n, const int64_t *part, const int6
       } else if (d->nranks > 1 && !(d->flags & SHIRO_F_XCHG_NCCL)) {
         p2p_setup(pl, xchg);
       }
+      plan_drop_host(pl);
     }
     pl.info.plan_seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -870,7 +935,29 @@ int shiro_plan_loopback(int32_t nranks, int32_t group_size, uint32_t flags, int6
         auto flag = [&](int d, int i) -> int32_t * { return h->ranks[d]->route.xflags + i; };
         hier_resolve(pl, seg, flag);
       }
+    } else if (!host_only && P > 1 && !(flags & SHIRO_F_XCHG_NCCL)) {
+      // fused producer launch with same-device destinations (the kernels of
+      // the NVLink path); SHIRO_F_XCHG_NCCL keeps the staged copy exchange
+      for (int r = 0; r < P; ++r) {
+        Plan &pl = *h->ranks[r];
+        const int64_t rowb = (int64_t)pl.N * sizeof(float);
+        std::vector<uint64_t> dstp, outp;
+        for (int d = 0; d < P; ++d) {
+          if (d == r) continue;
+          Plan &D = *h->ranks[d];
+          char *base = reinterpret_cast<char *>(D.recv_buf) + D.recv_off[r] * rowb;
+          for (size_t k = 0; k < pl.send_b[d].size(); ++k)
+            dstp.push_back((uint64_t)(base + (int64_t)k * rowb));
+          const int64_t nb = (int64_t)pl.send_b[d].size();
+          for (size_t k = 0; k < pl.send_c[d].size(); ++k)
+            outp.push_back((uint64_t)(base + (nb + (int64_t)k) * rowb));
+        }
+        upload_prod(pl, dstp, outp);
+        pl.p2p = true;      // marks the pointer-routed path (no flags in loopback)
+      }
     }
+    if (!host_only)
+      for (int r = 0; r < P; ++r) plan_drop_host(*h->ranks[r]);
     *out = h.release();
   });
 }
@@ -947,6 +1034,13 @@ int shiro_spmm_loopback(shiro_plan_t plan, const float *B, float *C, void *strea
       for (int r = 0; r < P; ++r) launches += stage_local(*plan->ranks[r], Bp(r), Cp(r), s);
       for (int r = 0; r < P; ++r) launches += hier_stage(*plan->ranks[r], 2, Bp(r), Cp(r), s);
       for (int r = 0; r < P; ++r) launches += hier_stage(*plan->ranks[r], 3, Bp(r), Cp(r), s);
+    } else if (plan->ranks[0]->p2p) {
+      // fused producer launches (peer rows + local rows), then the receives
+      for (int r = 0; r < P; ++r) {
+        Plan &pl = *plan->ranks[r];
+        launches += run_spmm(pl.d_prod, Bp(r), pl.M, nullptr, Cp(r), false, s);
+      }
+      for (int r = 0; r < P; ++r) launches += stage_recv(*plan->ranks[r], Cp(r), s);
     } else {
       for (int r = 0; r < P; ++r) launches += stage_send(*plan->ranks[r], Bp(r), s);
       // exchange: device copies send(s -> r) into recv(r from s)

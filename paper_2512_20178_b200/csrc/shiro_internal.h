@@ -47,6 +47,7 @@ struct HostCsr {
   std::vector<int32_t> col;
   std::vector<float> val;       // empty = all ones
   std::vector<int32_t> out_row;
+  bool ptr_rows = false;        // rows addressed by per-row output pointers
   int64_t nnz() const { return (int64_t)col.size(); }
 };
 
@@ -164,9 +165,11 @@ struct Plan {
   int64_t recv_buf_off = 0, flags_off = 0;
   std::vector<void *> peer_base;      // opened IPC mappings
   void *p2p_arena = nullptr;
-  float *const *pack_dstp = nullptr;
   int32_t *const *ready_ptrs = nullptr, *const *consumed_ptrs = nullptr;
-  DevSpmm d_out_p2p;
+  // fused producer launch: pack rows (unit weight) + row-based partials, both
+  // stored into peers' receive buffers, + the local rows into C (K4+K3+K1)
+  DevSpmm d_prod;
+  void *prod_ops = nullptr;
   int32_t *err_host = nullptr;        // pinned copy of flags[2P]
   int64_t wait_timeout_ns = 20000000000LL;
   // device staging of B and C for shiro_spmm_host
@@ -221,6 +224,11 @@ int64_t hier_stage(Plan &pl, int stage, const float *B, float *C, cudaStream_t s
 void exec_flat(Plan &plan, const float *B, float *C, cudaStream_t s);
 // fused NVLink exchange (p2p_host.cpp): IPC setup (collective) and executor
 void p2p_setup(Plan &plan, const Alltoallv &xchg);
+// build + upload the fused producer op; pack_addr / part_addr are the
+// destination addresses of the packed B rows and of the A_out rows
+void upload_prod(Plan &plan, const std::vector<uint64_t> &pack_addr,
+                 const std::vector<uint64_t> &part_addr);
+void plan_drop_host(Plan &plan);
 void p2p_release(Plan &plan);
 void exec_p2p(Plan &plan, const float *B, float *C, cudaStream_t s);
 void exec_plan(Plan &plan, const float *B, float *C, cudaStream_t s);

@@ -1,7 +1,7 @@
 """Multi-GPU correctness of the distributed path (one process per GPU, NCCL).
 
     torchrun --nproc-per-node P --master-addr 127.0.0.1 --master-port 29511 \
-        scripts/dist_check.py --config c2 [--flags fused,colmax] [--int]
+        scripts/dist_check.py --config c2 [--flags split,colmax] [--int]
 
 Every rank plans with shiro_plan (NCCL plan-time exchange), runs shiro_spmm
 (NCCL all-to-allv), and rank 0 checks the gathered C against the CPU oracle
@@ -46,7 +46,7 @@ def main():
     rp_l, col_l, val_l = sh.local_rows(row_ptr, col, val, part, rank)
     flags = 0
     for f in filter(None, args.flags.split(",")):
-        flags |= {"fused": sh.F_FUSED_RECV, "colmax": sh.F_COVER_COLMAX, "col": sh.F_MODE_COL,
+        flags |= {"split": sh.F_SPLIT_RECV, "colmax": sh.F_COVER_COLMAX, "col": sh.F_MODE_COL,
                   "row": sh.F_MODE_ROW, "nooverlap": sh.F_NO_OVERLAP, "nccl": sh.F_XCHG_NCCL}[f]
     obj = [sh.get_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
