@@ -56,13 +56,15 @@ int launch_pack(int64_t n, const int32_t *src, const int32_t *dst, const float *
 int launch_pack_ptr(int64_t n, const int32_t *src, float *const *dstp, const float *X, int32_t N,
                     cudaStream_t s);
 
-// Fused-exchange synchronisation over NVLink (p2p.cu).  signal: for each i,
-// st.release.sys *flags[i] = value (flags[i] may be a peer address).  wait:
-// spin until every local flags[i] >= value (ld.acquire.sys); after
-// timeout_ns sets *err = 1 and gives up instead of hanging the GPU.
-int launch_signal(int32_t *const *flags, int n, int32_t value, cudaStream_t s);
-int launch_wait(const int32_t *flags, int n, int32_t value, int32_t *err, int64_t timeout_ns,
-                cudaStream_t s);
+// Fused-exchange synchronisation over NVLink (p2p.cu), value = *epoch + add
+// read on the device.  signal: for each i, st.release.sys *flags[i] = value
+// (flags[i] may be a peer address); bump: then *epoch = value.  wait: spin
+// until every local flags[i] >= value (ld.acquire.sys); after timeout_ns sets
+// *err = 1 and gives up instead of hanging the GPU.
+int launch_signal(int32_t *const *flags, int n, int32_t *epoch, int add, bool bump,
+                  cudaStream_t s);
+int launch_wait(const int32_t *flags, int n, const int32_t *epoch, int add, int32_t *err,
+                int64_t timeout_ns, cudaStream_t s);
 
 // K5: C[tgt[u]] += sum_{k in [ptr[u], ptr[u+1])} R[src[k]] (gather-sum of
 // received partial C rows, fixed order: C first, then sources ascending)

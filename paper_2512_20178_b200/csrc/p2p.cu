@@ -31,15 +31,24 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
-__global__ void k_signal(int32_t *const *flags, int n, int32_t value) {
+// value = *epoch + add (the device-side epoch keeps the arguments of a
+// captured CUDA graph static); bump: advance the epoch afterwards (last
+// signal of a call).
+__global__ void k_signal(int32_t *const *flags, int n, int32_t *epoch, int add, int bump) {
   const int i = threadIdx.x;
+  const int32_t value = *epoch + add;
   __threadfence_system();
   if (i < n) st_release_sys(flags[i], value);
+  if (bump) {
+    __syncthreads();
+    if (i == 0) *epoch = value;
+  }
 }
 
-__global__ void k_wait(const int32_t *flags, int n, int32_t value, int32_t *err,
+__global__ void k_wait(const int32_t *flags, int n, const int32_t *epoch, int add, int32_t *err,
                        int64_t timeout_ns) {
   const int i = threadIdx.x;
+  const int32_t value = *epoch + add;
   if (i < n) {
     const uint64_t t0 = globaltimer();
     while (ld_acquire_sys(flags + i) < value) {
@@ -56,16 +65,17 @@ __global__ void k_wait(const int32_t *flags, int n, int32_t value, int32_t *err,
 
 }  // namespace
 
-int launch_signal(int32_t *const *flags, int n, int32_t value, cudaStream_t s) {
-  if (n <= 0) return 0;
-  k_signal<<<1, 64, 0, s>>>(flags, n, value);
+int launch_signal(int32_t *const *flags, int n, int32_t *epoch, int add, bool bump,
+                  cudaStream_t s) {
+  if (n <= 0 && !bump) return 0;
+  k_signal<<<1, 64, 0, s>>>(flags, n, epoch, add, bump ? 1 : 0);
   return 1;
 }
 
-int launch_wait(const int32_t *flags, int n, int32_t value, int32_t *err, int64_t timeout_ns,
-                cudaStream_t s) {
+int launch_wait(const int32_t *flags, int n, const int32_t *epoch, int add, int32_t *err,
+                int64_t timeout_ns, cudaStream_t s) {
   if (n <= 0) return 0;
-  k_wait<<<1, 64, 0, s>>>(flags, n, value, err, timeout_ns);
+  k_wait<<<1, 64, 0, s>>>(flags, n, epoch, add, err, timeout_ns);
   return 1;
 }
 

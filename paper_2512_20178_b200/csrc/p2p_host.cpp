@@ -117,7 +117,7 @@ void p2p_setup(Plan &pl, const Alltoallv &xchg) {
   pl.ready_ptrs = reinterpret_cast<int32_t *const *>(a);
   pl.consumed_ptrs = reinterpret_cast<int32_t *const *>(a + rdy.size());
   // 5. local flags: own entries never block (INT_MAX), the rest start at 0
-  std::vector<int32_t> f(2 * P + 1, 0);
+  std::vector<int32_t> f(2 * P + 2, 0);
   f[me] = INT_MAX;
   f[P + me] = INT_MAX;
   SHIRO_CK(cudaMemcpy(pl.xflags, f.data(), f.size() * sizeof(int32_t), cudaMemcpyHostToDevice));

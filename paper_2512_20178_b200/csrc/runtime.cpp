@@ -24,6 +24,7 @@ namespace shiro {
 
 Plan::~Plan() {
   if (!loopback_view) {
+    if (graph) cudaGraphExecDestroy(graph);
     p2p_release(*this);
     hier_release(*this);
     if (comm) ncclCommDestroy(comm);
@@ -181,7 +182,7 @@ void plan_upload(Plan &pl, cudaStream_t s) {
   const size_t o_send = ar.reserve((size_t)pl.send_rows * N * sizeof(float));
   const size_t o_recv = ar.reserve((size_t)pl.recv_rows * N * sizeof(float));
   // fused-exchange flags: ready[P], consumed[P], err (IPC-exported with the arena)
-  const size_t o_flags = ar.reserve((2 * (size_t)pl.P + 1) * sizeof(int32_t));
+  const size_t o_flags = ar.reserve((2 * (size_t)pl.P + 2) * sizeof(int32_t));
   const bool fused = !(pl.flags & SHIRO_F_SPLIT_RECV);
   SpmmLayout l_diag = layout_spmm(ar, pl.A_diag, N);
   SpmmLayout l_out = layout_spmm(ar, pl.A_out, N);
@@ -421,7 +422,7 @@ void hier_upload(Plan &pl) {
   const int N = pl.N, P = pl.P;
   Arena ab;
   const size_t o_rb = ab.reserve((size_t)(R.r1_rows + R.r2_rows) * N * sizeof(float));
-  const size_t o_fl = ab.reserve((3 * (size_t)P + 1) * sizeof(int32_t));
+  const size_t o_fl = ab.reserve((3 * (size_t)P + 2) * sizeof(int32_t));
   SHIRO_CK(cudaMalloc(&R.arena, std::max<size_t>(ab.total, 256)));
   SHIRO_CK(cudaMemset(R.arena, 0, std::max<size_t>(ab.total, 256)));
   char *bb = static_cast<char *>(R.arena);
@@ -481,7 +482,7 @@ void hier_resolve(Plan &pl, const std::function<char *(int, int)> &seg,
   R.ready2_ptrs = reinterpret_cast<int32_t *const *>(a + o); o += P - 1;
   R.consumed_ptrs = reinterpret_cast<int32_t *const *>(a + o);
   // own flags never block
-  std::vector<int32_t> f(3 * P + 1, 0);
+  std::vector<int32_t> f(3 * P + 2, 0);
   f[me] = f[P + me] = f[2 * P + me] = 0x7fffffff;
   SHIRO_CK(cudaMemcpy(R.xflags, f.data(), f.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
 }
@@ -511,26 +512,25 @@ void exec_hier(Plan &pl, const float *B, float *C, cudaStream_t s) {
     if (pl.prof_on) SHIRO_CK(cudaEventRecord(pl.prof[i], s));
   };
   const int P = pl.P;
-  const int32_t e = ++pl.epoch;
-  int32_t *err = R.xflags + 3 * P;
+  int32_t *err = R.xflags + 3 * P, *ep = R.xflags + 3 * P + 1;   // device epoch e-1
   int64_t n = 0;
   rec(0);
-  n += launch_wait(R.xflags + 2 * P, P, e - 1, err, pl.wait_timeout_ns, s);
+  n += launch_wait(R.xflags + 2 * P, P, ep, 0, err, pl.wait_timeout_ns, s);   // CONSUMED >= e-1
   n += hier_stage(pl, 1, B, C, s);                        // Stage I producers
-  n += launch_signal(R.ready1_ptrs, P - 1, e, s);
+  n += launch_signal(R.ready1_ptrs, P - 1, ep, 1, false, s);
   rec(1);
   n += stage_local(pl, B, C, s);                          // K1
   rec(2);
-  n += launch_wait(R.xflags, P, e, err, pl.wait_timeout_ns, s);
+  n += launch_wait(R.xflags, P, ep, 1, err, pl.wait_timeout_ns, s);
   rec(3);
   n += hier_stage(pl, 2, B, C, s);                        // Stage II producers
-  n += launch_signal(R.ready2_ptrs, P - 1, e, s);
+  n += launch_signal(R.ready2_ptrs, P - 1, ep, 1, false, s);
   rec(4);
-  n += launch_wait(R.xflags + P, P, e, err, pl.wait_timeout_ns, s);
+  n += launch_wait(R.xflags + P, P, ep, 1, err, pl.wait_timeout_ns, s);
   rec(5);
   n += hier_stage(pl, 3, B, C, s);                        // final remote SpMM
   rec(6);
-  n += launch_signal(R.consumed_ptrs, P - 1, e, s);
+  n += launch_signal(R.consumed_ptrs, P - 1, ep, 1, true, s);   // ... and advance the epoch
   SHIRO_CK(cudaMemcpyAsync(pl.err_host, err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   pl.last_launches = n;
   pl.prof_used = 4;
@@ -550,19 +550,18 @@ void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
     if (pl.prof_on) SHIRO_CK(cudaEventRecord(pl.prof[i], s));
   };
   const int P = pl.P;
-  const int32_t e = ++pl.epoch;
-  int32_t *err = pl.xflags + 2 * P;
+  int32_t *err = pl.xflags + 2 * P, *ep = pl.xflags + 2 * P + 1;  // device epoch e-1
   int64_t launches = 0;
   rec(0);
-  launches += launch_wait(pl.xflags + P, P, e - 1, err, pl.wait_timeout_ns, s);
+  launches += launch_wait(pl.xflags + P, P, ep, 0, err, pl.wait_timeout_ns, s);
   rec(1);
   rec(2);
   rec(5);
   launches += run_spmm(pl.d_prod, B, pl.M, nullptr, C, false, s);
   rec(6);
-  launches += launch_signal(pl.ready_ptrs, P - 1, e, s);
+  launches += launch_signal(pl.ready_ptrs, P - 1, ep, 1, false, s);
   rec(3);
-  launches += launch_wait(pl.xflags, P, e, err, pl.wait_timeout_ns, s);
+  launches += launch_wait(pl.xflags, P, ep, 1, err, pl.wait_timeout_ns, s);
   rec(4);
   if (!(pl.flags & SHIRO_F_SPLIT_RECV)) {
     launches += run_spmm(pl.d_rem, pl.recv_buf, pl.recv_rows, nullptr, C, true, s);
@@ -574,7 +573,7 @@ void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
                                    pl.d_scatter.src, pl.recv_buf, C, pl.N, s);
   }
   rec(8);
-  launches += launch_signal(pl.consumed_ptrs, P - 1, e, s);
+  launches += launch_signal(pl.consumed_ptrs, P - 1, ep, 1, true, s);
   SHIRO_CK(cudaMemcpyAsync(pl.err_host, err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   pl.last_launches = launches;
   pl.prof_used = 3;
@@ -606,6 +605,53 @@ struct shiro_plan_s {
 namespace {
 
 thread_local std::string g_last_error;
+
+// A step is captured into a CUDA graph (and replayed while B, C, the stream
+// and the profiling state are unchanged) for the paths whose launches have
+// static arguments: P = 1, the fused exchange and the hierarchical schedule
+// (their epochs live on the device).  Not on the legacy default stream (it
+// cannot be captured), not for the NCCL exchange; SHIRO_GRAPH=0 disables.
+bool graph_eligible(const Plan &pl, cudaStream_t s) {
+  static int env = -1;
+  if (env < 0) {
+    const char *e = getenv("SHIRO_GRAPH");
+    env = (e && e[0] == '0') ? 0 : 1;
+  }
+  if (!env || s == nullptr || s == cudaStreamLegacy || s == cudaStreamPerThread) return false;
+  if (pl.prof_on) return false;      // stage events need direct launches
+  return pl.P == 1 || pl.p2p || pl.route.active;
+}
+
+void launch_graph(Plan &pl, const float *B, float *C, cudaStream_t s) {
+  if (pl.err_host && *pl.err_host)
+    throw Error(SHIRO_E_PEER, "fused exchange: a peer did not signal in time");
+  if (!pl.graph || pl.g_B != B || pl.g_C != C || pl.g_s != s || pl.g_prof != pl.prof_on) {
+    if (pl.graph) {
+      cudaGraphExecDestroy(pl.graph);
+      pl.graph = nullptr;
+    }
+    SHIRO_CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    cudaGraph_t g = nullptr;
+    try {
+      exec_plan(pl, B, C, s);
+    } catch (...) {
+      cudaStreamEndCapture(s, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    SHIRO_CK(cudaStreamEndCapture(s, &g));
+    const cudaError_t ie = cudaGraphInstantiate(&pl.graph, g, 0);
+    cudaGraphDestroy(g);
+    SHIRO_CK(ie);
+    pl.g_B = B;
+    pl.g_C = C;
+    pl.g_s = s;
+    pl.g_prof = pl.prof_on;
+    pl.g_launches = pl.last_launches;
+  }
+  SHIRO_CK(cudaGraphLaunch(pl.graph, s));
+  pl.last_launches = pl.g_launches;
+}
 
 int fail(const Error &e) {
   g_last_error = e.msg;
@@ -993,7 +1039,12 @@ int shiro_spmm(shiro_plan_t plan, const float *B_p, float *C_p, void *stream) {
       if (as != ncclSuccess && as != ncclInProgress)
         throw Error(SHIRO_E_NCCL, std::string("asynchronous NCCL error: ") + ncclGetErrorString(as));
     }
-    exec_plan(pl, B_p, C_p, static_cast<cudaStream_t>(stream));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (graph_eligible(pl, s)) {
+      launch_graph(pl, B_p, C_p, s);
+    } else {
+      exec_plan(pl, B_p, C_p, s);
+    }
     SHIRO_CK(cudaGetLastError());
     plan->last_launches = pl.last_launches;
   });

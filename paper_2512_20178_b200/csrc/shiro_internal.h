@@ -172,6 +172,14 @@ struct Plan {
   void *prod_ops = nullptr;
   int32_t *err_host = nullptr;        // pinned copy of flags[2P]
   int64_t wait_timeout_ns = 20000000000LL;
+  // CUDA graph of one step (P = 1, fused exchange, hierarchical), keyed by
+  // (B, C, stream, profiling); replayed while the key matches
+  cudaGraphExec_t graph = nullptr;
+  const float *g_B = nullptr;
+  float *g_C = nullptr;
+  cudaStream_t g_s = nullptr;
+  bool g_prof = false;
+  int64_t g_launches = 0;
   // device staging of B and C for shiro_spmm_host
   float *stage = nullptr;
 
