@@ -279,7 +279,7 @@ def main():
         if world > 1:
             dist.barrier()
 
-    row_ptr, col, val = shiro_gen.gen_matrix(cfg, cache_dir=_cache_dir())
+    row_ptr, col, val = shiro_gen.gen_matrix_shared(cfg, rank, barrier, cache_dir=_cache_dir())
     nnz = int(row_ptr[-1])
     part = sh.uniform_partition(cfg.n, world)
     lo, hi = int(part[rank]), int(part[rank + 1])

@@ -12,7 +12,7 @@ for a in "--config c2" "--config c2 --int --flags split" "--config c2 --int --fl
   SHIRO_P2P_TIMEOUT_MS=20000 timeout 300 $TR scripts/dist_check.py $a >> $OUT 2>gpurun_out/multi_err_P$P.log || echo "FAILED rc=$?" >> $OUT
 done
 for c in $CFGS; do
-  for opt in "--xchg p2p" "--xchg nccl"; do
+  for opt in "--xchg p2p" "--group-size $GS"; do
     echo "== bench $c $opt" >> $OUT
     timeout 600 $TR bench.py --gpus $P --config $c --steps 10 --warmup 3 --no-e2e --no-cpu-baseline $opt >> $OUT 2>>gpurun_out/multi_err_P$P.log || echo "FAILED rc=$?" >> $OUT
   done

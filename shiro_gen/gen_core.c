@@ -10,6 +10,8 @@
  * Build: gcc -O2 -fopenmp -shared -fPIC gen_core.c -o libshirogen.so
  */
 #include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
 
 static inline uint64_t mix64(uint64_t z) {
   z += 0x9e3779b97f4a7c15ULL;
@@ -106,3 +108,95 @@ void gen_fill_B(uint64_t seed, int64_t row_lo, int64_t nrows, int64_t N,
     }
   }
 }
+
+/* Directed R-MAT CSR for very large configs (c5), without materialising the
+ * samples: pass 1 counts samples per (scrambled) row, pass 2 regenerates the
+ * same counter-based samples and scatters their columns, then every row is
+ * sorted and deduplicated.  Result = the distinct entries among samples
+ * 0..m-1 (Graph500 convention: m = edge factor x n samples).  perm: old id ->
+ * new id (scrambling), or NULL.  Outputs: row_ptr[n+1] (caller-allocated),
+ * *col_out (malloc'd, int32, length *nnz_out).  Deterministic, independent of
+ * the thread count.  Returns 0 on success. */
+static int cmp_i32(const void *a, const void *b) {
+  int32_t x = *(const int32_t *)a, y = *(const int32_t *)b;
+  return (x > y) - (x < y);
+}
+
+int gen_rmat_csr(uint64_t seed, int64_t m, int32_t levels, double a, double b, double c,
+                 int64_t n, const int64_t *perm, int64_t *row_ptr, int32_t **col_out,
+                 int64_t *nnz_out) {
+  int64_t *cnt = calloc(n + 1, sizeof(int64_t));
+  if (!cnt) return 1;
+  const int64_t CH = 1 << 22;
+  int64_t k0;
+  /* pass 1: counts */
+#pragma omp parallel for schedule(dynamic, 1)
+  for (k0 = 0; k0 < m; k0 += CH) {
+    int64_t e = k0 + CH < m ? k0 + CH : m;
+    for (int64_t k = k0; k < e; k++) {
+      int64_t i = 0, j = 0;
+      for (int32_t l = 0; l < levels; l++) {
+        double u = u53(gen_hash(seed, ST_RMAT + (uint64_t)l, (uint64_t)k));
+        int rb = (u >= a + b) ? 1 : 0;
+        int cb = (u >= a && u < a + b) || (u >= a + b + c) ? 1 : 0;
+        i = (i << 1) | rb;
+        j = (j << 1) | cb;
+      }
+      if (i >= n || j >= n) continue;
+      if (perm) i = perm[i];
+#pragma omp atomic
+      cnt[i + 1]++;
+    }
+  }
+  for (int64_t r = 0; r < n; r++) cnt[r + 1] += cnt[r];
+  const int64_t total = cnt[n];
+  int32_t *col = malloc(sizeof(int32_t) * (total > 0 ? total : 1));
+  int64_t *fill = malloc(sizeof(int64_t) * (n > 0 ? n : 1));
+  if (!col || !fill) return 1;
+  memcpy(fill, cnt, sizeof(int64_t) * n);
+  /* pass 2: scatter columns (order inside a row fixed by the sort below) */
+#pragma omp parallel for schedule(dynamic, 1)
+  for (k0 = 0; k0 < m; k0 += CH) {
+    int64_t e = k0 + CH < m ? k0 + CH : m;
+    for (int64_t k = k0; k < e; k++) {
+      int64_t i = 0, j = 0;
+      for (int32_t l = 0; l < levels; l++) {
+        double u = u53(gen_hash(seed, ST_RMAT + (uint64_t)l, (uint64_t)k));
+        int rb = (u >= a + b) ? 1 : 0;
+        int cb = (u >= a && u < a + b) || (u >= a + b + c) ? 1 : 0;
+        i = (i << 1) | rb;
+        j = (j << 1) | cb;
+      }
+      if (i >= n || j >= n) continue;
+      if (perm) { i = perm[i]; j = perm[j]; }
+      int64_t pos;
+#pragma omp atomic capture
+      pos = fill[i]++;
+      col[pos] = (int32_t)j;
+    }
+  }
+  free(fill);
+  /* sort + dedup every row, compact in place row by row */
+  int64_t *keep = malloc(sizeof(int64_t) * (n > 0 ? n : 1));
+  int64_t r;
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (r = 0; r < n; r++) {
+    int32_t *p = col + cnt[r];
+    int64_t len = cnt[r + 1] - cnt[r], w = 0;
+    if (len > 1) qsort(p, (size_t)len, sizeof(int32_t), cmp_i32);
+    for (int64_t t = 0; t < len; t++)
+      if (t == 0 || p[t] != p[t - 1]) p[w++] = p[t];
+    keep[r] = w;
+  }
+  row_ptr[0] = 0;
+  for (r = 0; r < n; r++) row_ptr[r + 1] = row_ptr[r] + keep[r];
+  for (r = 0; r < n; r++)      /* compact (sequential: destinations never pass sources) */
+    if (row_ptr[r] != cnt[r]) memmove(col + row_ptr[r], col + cnt[r], sizeof(int32_t) * keep[r]);
+  free(keep);
+  free(cnt);
+  *nnz_out = row_ptr[n];
+  *col_out = realloc(col, sizeof(int32_t) * (row_ptr[n] > 0 ? row_ptr[n] : 1));
+  return 0;
+}
+
+void gen_free(void *p) { free(p); }
