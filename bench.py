@@ -378,7 +378,8 @@ def main():
     # gather-aware roofline: the dominant local op's own column stream through
     # the pure gather probe, plus uniform-random gathers from an L2-resident
     # (32 MiB) and an HBM-resident (4 GiB) table
-    gather = gather_probes(sh, torch, dev, stream, Bd, rp_l, col_l, lo, hi, cfg.N, flush)
+    gather = gather_probes(sh, torch, dev, stream, Bd, rp_l, col_l, lo, hi, cfg.N, flush) \
+        if world == 1 else None      # at P > 1 the dominant launch also carries peer rows
     if gather and dom == "local":
         roof["gather_floor_ms"] = gather["csr_stream_ms"]
         roof["gather_frac"] = round(gather["csr_stream_ms"] / dom_ms, 4)
