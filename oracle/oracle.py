@@ -225,6 +225,8 @@ def plan_flat(n, part, row_ptr, col, mode="joint", rule="rowmax") -> FlatPlan:
       selected else ROW (R2: doubly covered nonzeros follow the rule side).
     col:   every off-diagonal nonzero COL (Eq. 2).
     row:   every off-diagonal nonzero ROW (Eq. 3).
+    block: sparsity-oblivious, q sends its whole B row block to every p with
+           a non-empty A^(p,q) (Eq. 1); all nonzeros COL.
     Lists: send_b[(q,p)] = selected cols, send_c[(q,p)] = selected rows,
     global ids ascending."""
     part = np.asarray(part, np.int64)
@@ -263,11 +265,15 @@ def plan_flat(n, part, row_ptr, col, mode="joint", rule="rowmax") -> FlatPlan:
                 is_row = np.zeros(idx.size, bool)
             elif mode == "row":
                 is_row = np.ones(idx.size, bool)
+            elif mode == "block":
+                is_row = np.zeros(idx.size, bool)
             else:
                 raise ValueError(mode)
             tag[idx] = np.where(is_row, ROW, COL)
             plan.send_c[(q, p)] = np.unique(bi[is_row]).astype(np.int64)
             plan.send_b[(q, p)] = np.unique(bj[~is_row]).astype(np.int64)
+            if mode == "block":
+                plan.send_b[(q, p)] = np.arange(part[q], part[q + 1], dtype=np.int64)
             plan.nnz_row[(q, p)] = int(is_row.sum())
             if plan.send_c[(q, p)].size == 0:
                 del plan.send_c[(q, p)]

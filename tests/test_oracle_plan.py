@@ -113,3 +113,18 @@ def test_c1_config_bytes_below_oblivious():
         v = oracle.volumes(plan, cfg.N)
         assert v["joint_bytes"] < v["oblivious_bytes"]
         assert v["joint_rows"] <= min(v["col_rows"], v["row_rows"])
+
+
+def test_block_mode_is_eq1():
+    """Sparsity-oblivious block strategy (Eq. 1): per non-empty
+    block q sends all K_q rows; the executed product is still exact."""
+    rng = np.random.default_rng(77)
+    n, P = 120, 4
+    row_ptr, col, val = random_csr(rng, n, 0.03)
+    part = oracle.uniform_partition(n, P)
+    pb = oracle.plan_flat(n, part, row_ptr, col, mode="block")
+    v = oracle.volumes(pb, 8)
+    assert v["joint_rows"] == v["block_rows"]
+    B = rng.integers(0, 8, (n, 3)).astype(np.float32)
+    assert np.array_equal(oracle.exec_flat(pb, row_ptr, col, val, B),
+                          oracle.spmm_ref(row_ptr, col, val, B))
