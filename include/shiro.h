@@ -68,6 +68,8 @@ enum shiro_status {
                                           two launches; default: one fused pass  */
 #define SHIRO_F_HOST_ONLY (1u << 4)    /* plan lists/stats only, no device state */
 #define SHIRO_F_NO_OVERLAP (1u << 5)   /* local SpMM after the exchange (ablation)*/
+#define SHIRO_F_MODE_BLOCK (1u << 7)   /* sparsity-oblivious: whole B row block
+                                          per non-empty A^(p,q) (Eq. 1) */
 #define SHIRO_F_XCHG_NCCL (1u << 6)    /* exchange with NCCL grouped send/recv
                                           instead of the default fused exchange
                                           (K4/K3 store straight into the peers'

@@ -29,6 +29,7 @@ F_SPLIT_RECV = 1 << 3
 F_HOST_ONLY = 1 << 4
 F_NO_OVERLAP = 1 << 5
 F_XCHG_NCCL = 1 << 6
+F_MODE_BLOCK = 1 << 7
 
 STAGES = ("pack", "partial", "exchange", "local", "remote", "scatter", "total")
 

@@ -117,6 +117,7 @@ Phase1 plan_phase1(const PlanInput &in) {
   const bool colmax = in.flags & SHIRO_F_COVER_COLMAX;
   const bool mode_col = in.flags & SHIRO_F_MODE_COL;
   const bool mode_row = in.flags & SHIRO_F_MODE_ROW;
+  const bool mode_block = in.flags & SHIRO_F_MODE_BLOCK;   // Eq. 1: whole B blocks
   Phase1 p1;
   p1.out.assign(P, {});
   p1.tag.assign(nnz, 0);
@@ -175,7 +176,8 @@ Phase1 plan_phase1(const PlanInput &in) {
     ap.push_back(ne);
     const int32_t nr = (int32_t)urow.size(), nc = (int32_t)ucol.size();
     std::vector<uint8_t> sel_r, sel_c;
-    if (!mode_col && !mode_row) block_cover(nr, nc, ap, adj, colmax, sel_r, sel_c);
+    const bool joint = !mode_col && !mode_row && !mode_block;
+    if (joint) block_cover(nr, nc, ap, adj, colmax, sel_r, sel_c);
     // assignment (P3)
     std::vector<uint8_t> row_used(nr, 0), col_used(nc, 0);
     int64_t nrow_nz = 0;
@@ -183,7 +185,7 @@ Phase1 plan_phase1(const PlanInput &in) {
       for (int64_t e = ap[u]; e < ap[u + 1]; ++e) {
         const int32_t v = adj[e];
         bool is_row;
-        if (mode_col) is_row = false;
+        if (mode_col || mode_block) is_row = false;
         else if (mode_row) is_row = true;
         else if (!colmax) is_row = sel_r[u];
         else is_row = !sel_c[v];
@@ -194,10 +196,12 @@ Phase1 plan_phase1(const PlanInput &in) {
       }
     std::vector<int64_t> b_ids, c_ids;
     for (int32_t v = 0; v < nc; ++v)
-      if (col_used[v]) b_ids.push_back(ucol[v]);
+      if (col_used[v] && !mode_block) b_ids.push_back(ucol[v]);
+    if (mode_block)
+      for (int64_t x = 0; x < Kq; ++x) b_ids.push_back(qlo + x);
     for (int32_t u = 0; u < nr; ++u)
       if (row_used[u]) c_ids.push_back(lo + urow[u]);
-    if (!mode_col && !mode_row) {
+    if (joint) {
       // every selected vertex carries a private edge (minimality)
       for (int32_t u = 0; u < nr; ++u)
         if (sel_r[u] != row_used[u]) throw Error(SHIRO_E_INTERNAL, "selected row unused");

@@ -49,7 +49,8 @@ def assert_stats_equal(pl, op, N, g=1):
 
 
 FLAGS = {("joint", "rowmax"): 0, ("joint", "colmax"): sh.F_COVER_COLMAX,
-         ("col", "rowmax"): sh.F_MODE_COL, ("row", "rowmax"): sh.F_MODE_ROW}
+         ("col", "rowmax"): sh.F_MODE_COL, ("row", "rowmax"): sh.F_MODE_ROW,
+         ("block", "rowmax"): sh.F_MODE_BLOCK}
 
 
 @pytest.mark.parametrize("seed", range(40))
@@ -59,7 +60,7 @@ def test_random_matrices(seed):
     P = [1, 2, 3, 4, 8][seed % 5]
     row_ptr, col, val = random_csr(rng, n, float(rng.uniform(0.003, 0.2)), symmetric=seed % 3 == 0)
     part = oracle.uniform_partition(n, P)
-    mode, rule = list(FLAGS)[seed % 4]
+    mode, rule = list(FLAGS)[seed % 5]
     pl = sh.Plan.loopback(P, n, part, row_ptr, col, val, 16, flags=FLAGS[(mode, rule)] | sh.F_HOST_ONLY)
     op = oracle.plan_flat(n, part, row_ptr, col, mode=mode, rule=rule)
     assert_lists_equal(pl, op, P)
