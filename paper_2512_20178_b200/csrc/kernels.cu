@@ -23,6 +23,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "kernels.h"
 
 namespace shiro {
@@ -507,7 +509,119 @@ void scatter_shape(int64_t nt, const int32_t *tgt, const int64_t *ptr, const int
     else FN<32, 4>(__VA_ARGS__);                          \
   } while (0)
 
+// ---------------------------------------------------------------------------
+// Fused step kernel: compute -> NVLink exchange -> compute in ONE launch.
+// Persistent lane groups pull producer units (K4 pack rows, K3 partial rows
+// stored into the peers' receive buffers, K1 local rows into C) from a
+// counter; the lane group completing the last producer unit raises READY at
+// every peer (after every unit's stores were fenced at system scope).  Lane
+// groups that run out of producer work wait until every peer's READY and
+// this GPU's own producer count are complete, then pull remote units (K2 +
+// K5 fused, accumulating into C).  Producer units are all claimed by running
+// lane groups before anyone waits, so non-resident CTAs cannot deadlock the
+// step; waits time out into an error flag instead of hanging the GPU.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void st_release_sys_i32(int32_t *p, int32_t v) {
+  asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int32_t ld_acquire_sys_i32(const int32_t *p) {
+  int32_t v;
+  asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int32_t ld_acquire_gpu_i32(const int32_t *p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <int LPR, int VPL, int MINB, int U>
+__global__ void __launch_bounds__(kBlock, MINB) k_step(const StepArgs s) {
+  const int lane = threadIdx.x & 31;
+  const int sub = lane / LPR;
+  const int li = lane % LPR;
+  const unsigned mask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (sub * LPR));
+  const int totA = s.prod.n_tasks + s.prod.n_groups;
+  const int totB = s.rem.n_tasks + s.rem.n_groups;
+  const int32_t e = *s.epoch + 1;
+  auto signal_ready = [&]() {
+    __threadfence_system();
+    for (int i = li; i < s.n_peers; i += LPR) st_release_sys_i32(s.ready_ptrs[i], e);
+  };
+  // ---- phase A: producer units, static grid-stride assignment ---------------
+  const int R = 32 / LPR;
+  const int64_t nlg = (int64_t)gridDim.x * (kBlock / 32) * R;          // lane groups
+  const int64_t lg = (((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5) * R + sub;
+  for (int64_t u = lg; u < totA; u += nlg)
+    spmm_unit<LPR, VPL, false, false, (U < LPR ? U : LPR), true>(s.prod, u, li, mask);
+  // one system-scope fence + one completion count per lane group; the last
+  // lane group raises READY at every peer
+  __threadfence_system();
+  __syncwarp(mask);
+  {
+    int done = 0;
+    if (li == 0) done = atomicAdd(s.ctr + 1, 1);
+    done = __shfl_sync(mask, done, 0, LPR);
+    if (done == nlg - 1) signal_ready();
+  }
+  // ---- wait: own producers complete, every peer READY ----------------------
+  {
+    const uint64_t t0 = gtimer();
+    bool ok = true;
+    for (;;) {
+      bool ready = ld_acquire_gpu_i32(s.ctr + 1) >= nlg;
+      for (int i = li; i < s.P && ready; i += LPR) ready = ld_acquire_sys_i32(s.ready_local + i) >= e;
+      ready = __all_sync(mask, ready);
+      if (ready) break;
+      if ((int64_t)(gtimer() - t0) > s.timeout_ns) { ok = false; break; }
+      __nanosleep(128);
+    }
+    if (!ok) {
+      if (li == 0) atomicExch(s.err, 1);
+      return;
+    }
+  }
+  // ---- phase B: remote units (accumulate), static grid-stride --------------
+  for (int64_t u = lg; u < totB; u += nlg)
+    spmm_unit<LPR, VPL, true, false, (U < LPR ? U : LPR), false>(s.rem, u, li, mask);
+}
+
+template <int LPR, int VPL>
+void step_shape(const StepArgs &s, cudaStream_t st) {
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step<LPR, VPL, 5, 4>, kBlock, 0);
+    if (per_sm < 1) per_sm = 1;
+  }
+  const int64_t unitsA = s.prod.n_tasks + s.prod.n_groups, unitsB = s.rem.n_tasks + s.rem.n_groups;
+  const int64_t need = blocks_for(std::max<int64_t>(std::max(unitsA, unitsB), 1), 32 / LPR);
+  const int64_t grid = std::min<int64_t>((int64_t)per_sm * num_sms(), need);
+  // cooperative launch: every CTA co-resident (lane groups wait on each other)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kBlock);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_step<LPR, VPL, 5, 4>, s);
+}
+
 }  // namespace
+
+int launch_step(const StepArgs &s, cudaStream_t st) {
+  int lpr, vpl;
+  if (!vec_shape(s.prod.N, &lpr, &vpl) || vpl != 1) return -1;   // caller falls back
+  SHIRO_DISPATCH(s.prod.N, step_shape, s, st);
+  return 1;
+}
 
 // Vector shape for width N: LPR lanes per row, VPL float4 per lane.
 bool vec_shape(int N, int *lpr, int *vpl) {

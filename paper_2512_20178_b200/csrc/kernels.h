@@ -52,6 +52,22 @@ int launch_spmm(const SpmmArgs &a, bool accumulate, cudaStream_t s);
 int launch_pack(int64_t n, const int32_t *src, const int32_t *dst, const float *X, float *Y,
                 int32_t N, cudaStream_t s);
 
+// Fused step (one launch): producer op (pointer-routed, overwrite) -> READY
+// to peers -> wait for peers -> remote op (accumulate into C).
+struct StepArgs {
+  SpmmArgs prod, rem;
+  int *ctr = nullptr;                   // [3] zeroed before the launch
+  int32_t *const *ready_ptrs = nullptr; // peers' READY flags for this rank
+  int n_peers = 0;
+  const int32_t *ready_local = nullptr; // [P] READY flags of this rank
+  int P = 0;
+  const int32_t *epoch = nullptr;       // device epoch (value e-1)
+  int32_t *err = nullptr;
+  int64_t timeout_ns = 0;
+};
+// returns launches issued, or -1 if the width has no fused-step shape
+int launch_step(const StepArgs &s, cudaStream_t st);
+
 // K4 into peer memory: dstp[i] is the (peer-mapped) address of packed row i
 int launch_pack_ptr(int64_t n, const int32_t *src, float *const *dstp, const float *X, int32_t N,
                     cudaStream_t s);

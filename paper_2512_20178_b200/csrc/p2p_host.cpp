@@ -107,8 +107,10 @@ void p2p_setup(Plan &pl, const Alltoallv &xchg) {
     throw Error(SHIRO_E_INTERNAL, "fused exchange: row count mismatch");
   upload_prod(pl, dstp, outp);          // K4 + K3 + K1 as one pointer-routed launch
   const size_t n_all = rdy.size() + cons.size();
-  SHIRO_CK(cudaMalloc(&pl.p2p_arena, std::max<size_t>(8, n_all * sizeof(uint64_t))));
+  // pointer arrays, then 2 x uint64 of fused-step work counters
+  SHIRO_CK(cudaMalloc(&pl.p2p_arena, (n_all + 2) * sizeof(uint64_t)));
   uint64_t *a = static_cast<uint64_t *>(pl.p2p_arena);
+  pl.step_ctr = reinterpret_cast<int *>(a + n_all);
   std::vector<uint64_t> all;
   all.insert(all.end(), rdy.begin(), rdy.end());
   all.insert(all.end(), cons.begin(), cons.end());

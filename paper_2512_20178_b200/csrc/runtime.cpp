@@ -544,6 +544,18 @@ void exec_hier(Plan &pl, const float *B, float *C, cudaStream_t s) {
 //   signal READY = e at peers
 //   wait READY >= e from all peers, K2 remote SpMM + K5 scatter-add (fused
 //   by default), signal CONSUMED = e at peers
+// SHIRO_FUSED_STEP=1 runs producer -> READY -> wait -> remote as ONE launch (k_step)
+bool fused_step_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    // opt-in: measured slower than graph-replayed separate launches at P=4
+    // (c4 1.36 vs 1.15 ms, profiles/r1_fused_step_P4.txt)
+    const char *e = getenv("SHIRO_FUSED_STEP");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
   if (*pl.err_host) throw Error(SHIRO_E_PEER, "fused exchange: a peer did not signal in time");
   auto rec = [&](int i) {
@@ -557,6 +569,33 @@ void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
   rec(1);
   rec(2);
   rec(5);
+  if (fused_step_enabled() && !(pl.flags & SHIRO_F_SPLIT_RECV) && pl.step_ctr) {
+    // one launch: producer -> READY -> wait -> remote (k_step)
+    StepArgs sa;
+    sa.prod = pl.d_prod.a;
+    sa.prod.X0 = B; sa.prod.n0 = pl.M; sa.prod.X1 = nullptr; sa.prod.Y = C;
+    sa.rem = pl.d_rem.a;
+    sa.rem.X0 = pl.recv_buf; sa.rem.n0 = pl.recv_rows; sa.rem.X1 = nullptr; sa.rem.Y = C;
+    sa.ctr = pl.step_ctr;
+    sa.ready_ptrs = pl.ready_ptrs;
+    sa.n_peers = P - 1;
+    sa.ready_local = pl.xflags;
+    sa.P = P;
+    sa.epoch = ep;
+    sa.err = err;
+    sa.timeout_ns = pl.wait_timeout_ns;
+    SHIRO_CK(cudaMemsetAsync(pl.step_ctr, 0, 4 * sizeof(int), s));
+    const int n = launch_step(sa, s);
+    if (n > 0) {
+      launches += n;
+      rec(6); rec(3); rec(4); rec(7); rec(8);
+      launches += launch_signal(pl.consumed_ptrs, P - 1, ep, 1, true, s);
+      SHIRO_CK(cudaMemcpyAsync(pl.err_host, err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      pl.last_launches = launches;
+      pl.prof_used = 3;
+      return;
+    }
+  }
   launches += run_spmm(pl.d_prod, B, pl.M, nullptr, C, false, s);
   rec(6);
   launches += launch_signal(pl.ready_ptrs, P - 1, ep, 1, false, s);

@@ -170,6 +170,7 @@ struct Plan {
   // stored into peers' receive buffers, + the local rows into C (K4+K3+K1)
   DevSpmm d_prod;
   void *prod_ops = nullptr;
+  int *step_ctr = nullptr;            // work counters of the fused step kernel
   int32_t *err_host = nullptr;        // pinned copy of flags[2P]
   int64_t wait_timeout_ns = 20000000000LL;
   // CUDA graph of one step (P = 1, fused exchange, hierarchical), keyed by

@@ -49,12 +49,16 @@ def main():
     Bd = torch.from_numpy(shiro_gen.gen_B(cfg.seed, lo, hi - lo, cfg.N)).to(dev)
     Cd = torch.empty_like(Bd)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    only = set(filter(None, os.environ.get("ABLATION_ONLY", "").split(",")))
     strategies = [("block", sh.F_MODE_BLOCK, 1), ("col", sh.F_MODE_COL, 1),
-                  ("row", sh.F_MODE_ROW, 1), ("joint", 0, 1)]
+                  ("row", sh.F_MODE_ROW, 1), ("joint", 0, 1),
+                  ("joint-colmax", sh.F_COVER_COLMAX, 1)]
     if args.group_size > 1 and world % args.group_size == 0 and world > args.group_size:
         strategies.append((f"joint+hier(g={args.group_size})", 0, args.group_size))
     records = []
     for name, flags, g in strategies:
+        if only and name.split("(")[0] not in only:
+            continue
         obj = [sh.get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         pl = sh.Plan.distributed(rank, world, cfg.n, part, rp_l, col_l, val_l, cfg.N,
