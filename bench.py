@@ -47,7 +47,8 @@ def load_peaks():
 
 # ----------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 100 ms."""
+    """nvidia-smi clocks + throttle reasons sampled every 50 ms (from the
+    warm-up through the timed region, the attribution pass and the e2e pass)."""
     Q = ("index,clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
@@ -61,7 +62,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms",
-                 "100", "-i", self.gpu], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                 "50", "-i", self.gpu], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
                 text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
@@ -334,7 +335,6 @@ def main():
         step_ms.append(ev[k][0].elapsed_time(ev[k][1]))
         launches += plan.last_launches()
     barrier()
-    clk = clocks.stop()
     # attribution pass: the same K steps with per-stage CUDA events (direct
     # launches on the same stream) -> which kernel dominates and its duration
     plan.profile(True)
@@ -429,6 +429,7 @@ def main():
                "d2h_bytes_per_step": int(M * cfg.N * 4) * world,
                "ms_per_step": round(te_mean * 1e3, 4)}
 
+    clk = clocks.stop()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         B_full = B_p if world == 1 else shiro_gen.gen_B(cfg.seed, 0, cfg.n, cfg.N)

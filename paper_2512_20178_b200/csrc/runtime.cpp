@@ -72,7 +72,7 @@ constexpr int32_t kChunk = 256, kChunkMin = 32;
 
 int32_t unit_size(int64_t nnz) {
   if (const char *e = getenv("SHIRO_CHUNK")) return std::max(kChunkMin, atoi(e));
-  int64_t L = nnz / ((int64_t)num_sms() * 64);
+  int64_t L = nnz / ((int64_t)num_sms() * 128);   // c2: 64 (swept 32..256), c3/c4: 256
   L = (L / 32) * 32;
   return (int32_t)std::max<int64_t>(kChunkMin, std::min<int64_t>(kChunk, L));
 }
