@@ -105,7 +105,7 @@ void p2p_setup(Plan &pl, const Alltoallv &xchg) {
   }
   if ((int64_t)outp.size() != pl.d_out.a.nrows || (int64_t)dstp.size() != pl.d_pack.n)
     throw Error(SHIRO_E_INTERNAL, "fused exchange: row count mismatch");
-  upload_prod(pl, dstp, outp);          // K4 + K3 + K1 as one pointer-routed launch
+  upload_prod(pl, pl.pack_src, dstp, outp);   // K4 + K3 + K1 as one pointer-routed launch
   const size_t n_all = rdy.size() + cons.size();
   // pointer arrays, then 2 x uint64 of fused-step work counters
   SHIRO_CK(cudaMalloc(&pl.p2p_arena, (n_all + 2) * sizeof(uint64_t)));

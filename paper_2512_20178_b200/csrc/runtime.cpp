@@ -260,15 +260,19 @@ void plan_drop_host(Plan &pl) {
 // (1) the packed B rows (one unit-weight nonzero each, K4), (2) the
 // row-based partial rows (A_out, K3) -- both stored at peer addresses -- and
 // (3) the local rows (A_diag, K1) stored into C (tagged row index).  Peer rows
-// come first so their NVLink stores start early.
-void upload_prod(Plan &pl, const std::vector<uint64_t> &pack_addr,
-                 const std::vector<uint64_t> &part_addr) {
+// come first so their NVLink stores start early.  The hierarchical schedule
+// uses the same launch for Stage I (its pack list holds the B-row unions).
+static bool prod_ops_exist(const Plan &pl) { return pl.prod_ops != nullptr; }
+
+void upload_prod(Plan &pl, const std::vector<int32_t> &pack_src,
+                 const std::vector<uint64_t> &pack_addr, const std::vector<uint64_t> &part_addr) {
   HostCsr c;
   c.ptr_rows = true;
   std::vector<uint64_t> outp;
-  const int64_t np = (int64_t)pl.pack_src.size();
+  const int64_t np = (int64_t)pack_src.size();
+  if (prod_ops_exist(pl)) { cudaFree(pl.prod_ops); pl.prod_ops = nullptr; }
   for (int64_t i = 0; i < np; ++i) {
-    c.col.push_back(pl.pack_src[i]);
+    c.col.push_back(pack_src[i]);
     c.val.push_back(1.0f);
     c.rp.push_back((int64_t)c.col.size());
     outp.push_back(pack_addr[i]);
@@ -485,6 +489,10 @@ void hier_resolve(Plan &pl, const std::function<char *(int, int)> &seg,
   std::vector<int32_t> f(3 * P + 2, 0);
   f[me] = f[P + me] = f[2 * P + me] = 0x7fffffff;
   SHIRO_CK(cudaMemcpy(R.xflags, f.data(), f.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  // Stage I producers + local rows as one launch (same as the flat fused exchange)
+  const size_t n1 = R.s1_pack_dst.size(), n2 = R.s1_part_dst.size();
+  upload_prod(pl, R.s1_pack_src, std::vector<uint64_t>(v.begin(), v.begin() + n1),
+              std::vector<uint64_t>(v.begin() + n1, v.begin() + n1 + n2));
 }
 
 // stage 1: B rows and partial C rows -> R1 (peers and self); stage 2: forward
@@ -516,10 +524,11 @@ void exec_hier(Plan &pl, const float *B, float *C, cudaStream_t s) {
   int64_t n = 0;
   rec(0);
   n += launch_wait(R.xflags + 2 * P, P, ep, 0, err, pl.wait_timeout_ns, s);   // CONSUMED >= e-1
-  n += hier_stage(pl, 1, B, C, s);                        // Stage I producers
-  n += launch_signal(R.ready1_ptrs, P - 1, ep, 1, false, s);
+  // Stage I producers (B-row unions, partial rows -> R1 of peers/self) and
+  // the local rows (K1 -> C) in one launch
+  n += run_spmm(pl.d_prod, B, pl.M, nullptr, C, false, s);
   rec(1);
-  n += stage_local(pl, B, C, s);                          // K1
+  n += launch_signal(R.ready1_ptrs, P - 1, ep, 1, false, s);
   rec(2);
   n += launch_wait(R.xflags, P, ep, 1, err, pl.wait_timeout_ns, s);
   rec(3);
@@ -1037,7 +1046,7 @@ int shiro_plan_loopback(int32_t nranks, int32_t group_size, uint32_t flags, int6
           for (size_t k = 0; k < pl.send_c[d].size(); ++k)
             outp.push_back((uint64_t)(base + (nb + (int64_t)k) * rowb));
         }
-        upload_prod(pl, dstp, outp);
+        upload_prod(pl, pl.pack_src, dstp, outp);
         pl.p2p = true;      // marks the pointer-routed path (no flags in loopback)
       }
     }
@@ -1120,8 +1129,10 @@ int shiro_spmm_loopback(shiro_plan_t plan, const float *B, float *C, void *strea
     if (P == 1) {
       launches += stage_local(*plan->ranks[0], Bp(0), Cp(0), s);
     } else if (plan->ranks[0]->route.active) {
-      for (int r = 0; r < P; ++r) launches += hier_stage(*plan->ranks[r], 1, Bp(r), Cp(r), s);
-      for (int r = 0; r < P; ++r) launches += stage_local(*plan->ranks[r], Bp(r), Cp(r), s);
+      for (int r = 0; r < P; ++r) {
+        Plan &pl = *plan->ranks[r];
+        launches += run_spmm(pl.d_prod, Bp(r), pl.M, nullptr, Cp(r), false, s);   // Stage I + K1
+      }
       for (int r = 0; r < P; ++r) launches += hier_stage(*plan->ranks[r], 2, Bp(r), Cp(r), s);
       for (int r = 0; r < P; ++r) launches += hier_stage(*plan->ranks[r], 3, Bp(r), Cp(r), s);
     } else if (plan->ranks[0]->p2p) {
@@ -1235,9 +1246,9 @@ int shiro_stage_times(shiro_plan_t plan, double *ms) {
       ms[SHIRO_STAGE_LOCAL] = ms[SHIRO_STAGE_TOTAL] = el(5, 6);
       return;
     }
-    if (pl.prof_used == 4) {   // hierarchical: PACK = Stage I, PARTIAL = Stage II producers
-      ms[SHIRO_STAGE_PACK] = el(0, 1);
-      ms[SHIRO_STAGE_LOCAL] = el(1, 2);
+    if (pl.prof_used == 4) {   // hierarchical: LOCAL = Stage I + K1 launch, PARTIAL = Stage II
+      ms[SHIRO_STAGE_LOCAL] = el(0, 1);
+      ms[SHIRO_STAGE_PACK] = el(1, 2);
       ms[SHIRO_STAGE_EXCHANGE] = el(2, 3) + el(4, 5);
       ms[SHIRO_STAGE_PARTIAL] = el(3, 4);
       ms[SHIRO_STAGE_REMOTE] = el(5, 6);

@@ -235,8 +235,8 @@ void exec_flat(Plan &plan, const float *B, float *C, cudaStream_t s);
 void p2p_setup(Plan &plan, const Alltoallv &xchg);
 // build + upload the fused producer op; pack_addr / part_addr are the
 // destination addresses of the packed B rows and of the A_out rows
-void upload_prod(Plan &plan, const std::vector<uint64_t> &pack_addr,
-                 const std::vector<uint64_t> &part_addr);
+void upload_prod(Plan &plan, const std::vector<int32_t> &pack_src,
+                 const std::vector<uint64_t> &pack_addr, const std::vector<uint64_t> &part_addr);
 void plan_drop_host(Plan &plan);
 void p2p_release(Plan &plan);
 void exec_p2p(Plan &plan, const float *B, float *C, cudaStream_t s);
