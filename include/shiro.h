@@ -70,6 +70,10 @@ enum shiro_status {
 #define SHIRO_F_NO_OVERLAP (1u << 5)   /* local SpMM after the exchange (ablation)*/
 #define SHIRO_F_MODE_BLOCK (1u << 7)   /* sparsity-oblivious: whole B row block
                                           per non-empty A^(p,q) (Eq. 1) */
+#define SHIRO_F_TRANSPOSE (1u << 8)    /* plan and run A^T (GNN backward, SURVEY
+                                          8(f) N3): the caller still passes its
+                                          rows of A; one distributed transpose at
+                                          plan time                              */
 #define SHIRO_F_XCHG_NCCL (1u << 6)    /* exchange with NCCL grouped send/recv
                                           instead of the default fused exchange
                                           (K4/K3 store straight into the peers'

@@ -30,6 +30,7 @@ F_HOST_ONLY = 1 << 4
 F_NO_OVERLAP = 1 << 5
 F_XCHG_NCCL = 1 << 6
 F_MODE_BLOCK = 1 << 7
+F_TRANSPOSE = 1 << 8
 
 STAGES = ("pack", "partial", "exchange", "local", "remote", "scatter", "total")
 

@@ -491,3 +491,64 @@ void plan_stats(const PlanInput &in, Plan &pl, const Alltoallv &xchg) {
 }
 
 }  // namespace shiro
+
+namespace shiro {
+
+// ---------------------------------------------------------------------------
+// Transposed SpMM (GNN backward C = A^T G): with
+// SHIRO_F_TRANSPOSE every rank passes its rows of A as usual; the entries are
+// redistributed once (entry (i, j) goes to the owner of j as (j, i)) and the
+// planner builds the joint plan of A^T, whose row blocks use the same
+// partition.  The transposed rows are sorted by column, so A^T is a valid CSR.
+// ---------------------------------------------------------------------------
+std::vector<std::vector<char>> transpose_messages(const PlanInput &in) {
+  const int P = in.P;
+  const int64_t lo = in.part[in.rank], M = in.part[in.rank + 1] - lo;
+  std::vector<std::vector<int64_t>> w(P);
+  for (int64_t t = 0; t < M; ++t)
+    for (int64_t k = in.row_ptr[t]; k < in.row_ptr[t + 1]; ++k) {
+      const int64_t j = in.col[k];
+      int q = 0;
+      while (in.part[q + 1] <= j) ++q;
+      int32_t bits;
+      std::memcpy(&bits, &in.val[k], 4);
+      w[q].push_back(j);
+      w[q].push_back(lo + t);
+      w[q].push_back(bits);
+    }
+  std::vector<std::vector<char>> out(P);
+  for (int q = 0; q < P; ++q) out[q] = to_bytes(w[q]);
+  return out;
+}
+
+void transpose_assemble(const PlanInput &in, const std::vector<std::vector<char>> &msgs,
+                        std::vector<int64_t> &rp, std::vector<int32_t> &col,
+                        std::vector<float> &val) {
+  const int64_t lo = in.part[in.rank], M = in.part[in.rank + 1] - lo;
+  std::vector<std::vector<std::pair<int32_t, float>>> rows(M);
+  for (const auto &b : msgs) {
+    const int64_t *w = reinterpret_cast<const int64_t *>(b.data());
+    const int64_t n3 = (int64_t)b.size() / 24;
+    for (int64_t e = 0; e < n3; ++e) {
+      const int64_t j = w[3 * e], i = w[3 * e + 1];
+      const int32_t bits = (int32_t)w[3 * e + 2];
+      float v;
+      std::memcpy(&v, &bits, 4);
+      if (j < lo || j >= lo + M) throw Error(SHIRO_E_INTERNAL, "transpose: misrouted entry");
+      rows[j - lo].push_back({(int32_t)i, v});
+    }
+  }
+  rp.assign(1, 0);
+  col.clear();
+  val.clear();
+  for (int64_t t = 0; t < M; ++t) {
+    std::sort(rows[t].begin(), rows[t].end(),
+              [](const std::pair<int32_t, float> &a, const std::pair<int32_t, float> &b) {
+                return a.first < b.first;
+              });
+    for (auto &e : rows[t]) { col.push_back(e.first); val.push_back(e.second); }
+    rp.push_back((int64_t)col.size());
+  }
+}
+
+}  // namespace shiro

@@ -901,6 +901,20 @@ int shiro_plan(const shiro_dist_t *d, int64_t n, const int64_t *part, const int6
     } else if (st) {
       throw Error(st, msg);
     }
+    // SHIRO_F_TRANSPOSE: plan A^T instead of A (one distributed transpose)
+    std::vector<int64_t> t_rp;
+    std::vector<int32_t> t_col;
+    std::vector<float> t_val;
+    if (d->flags & SHIRO_F_TRANSPOSE) {
+      std::vector<std::vector<char>> tmsg = transpose_messages(in), trecv;
+      xchg(tmsg, trecv);
+      trecv.resize(d->nranks);
+      trecv[d->rank] = tmsg[d->rank];
+      transpose_assemble(in, trecv, t_rp, t_col, t_val);
+      in.row_ptr = t_rp.data();
+      in.col = t_col.data();
+      in.val = t_val.data();
+    }
     // P2-P3
     Phase1 p1 = plan_phase1(in);
     // P4: one-time exchange of lists + A_row
@@ -949,10 +963,25 @@ int shiro_plan_loopback(int32_t nranks, int32_t group_size, uint32_t flags, int6
     auto h = std::make_unique<shiro_plan_s>();
     h->loopback = true;
     std::vector<PlanInput> ins(P);
+    std::vector<int64_t> lb_t_rp;      // full A^T for SHIRO_F_TRANSPOSE
+    std::vector<int32_t> lb_t_col;
+    std::vector<float> lb_t_val;
     std::vector<std::vector<int64_t>> rps(P);
     for (int r = 0; r < P; ++r) {
       PlanInput in{r, P, group_size, flags, n, part, nullptr, nullptr, nullptr, N};
       if (part[0] != 0 || part[P] != n) throw Error(SHIRO_E_PART, "part[0]/part[P] mismatch");
+      if (r == 0 && (flags & SHIRO_F_TRANSPOSE)) {
+        // full A^T on the host (validated as A first)
+        PlanInput all{0, 1, 1, 0, n, nullptr, row_ptr, col_idx, val, N};
+        const int64_t part1[2] = {0, n};
+        all.part = part1;
+        validate_input(all);
+        std::vector<std::vector<char>> one = transpose_messages(all);
+        transpose_assemble(all, one, lb_t_rp, lb_t_col, lb_t_val);
+        row_ptr = lb_t_rp.data();
+        col_idx = lb_t_col.data();
+        val = lb_t_val.data();
+      }
       for (int p = 0; p < P; ++p)
         if (part[p + 1] < part[p]) throw Error(SHIRO_E_PART, "part must be non-decreasing");
       const int64_t lo = part[r], hi = part[r + 1], base = row_ptr[lo];

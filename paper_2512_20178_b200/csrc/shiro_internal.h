@@ -243,3 +243,11 @@ void exec_p2p(Plan &plan, const float *B, float *C, cudaStream_t s);
 void exec_plan(Plan &plan, const float *B, float *C, cudaStream_t s);
 
 }  // namespace shiro
+
+namespace shiro {
+// distributed transpose for SHIRO_F_TRANSPOSE (plan.cpp)
+std::vector<std::vector<char>> transpose_messages(const PlanInput &in);
+void transpose_assemble(const PlanInput &in, const std::vector<std::vector<char>> &msgs,
+                        std::vector<int64_t> &rp, std::vector<int32_t> &col,
+                        std::vector<float> &val);
+}  // namespace shiro

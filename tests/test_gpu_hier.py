@@ -88,3 +88,21 @@ def test_graph_replay_matches_direct_launch():
         st.synchronize()
         assert np.array_equal(Cd.cpu().numpy().astype(np.float64), ref)
     assert pl.last_launches() == 1
+
+
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_transposed_product_integer_exact(P):
+    """SHIRO_F_TRANSPOSE computes C = A^T B (GNN backward)."""
+    from test_transpose import csr_transpose
+    rng = np.random.default_rng(31 + P)
+    n, N = 1200, 64
+    row_ptr, col, val = random_csr(rng, n, 0.01)
+    B = rng.integers(0, 8, (n, N)).astype(np.float32)
+    part = oracle.uniform_partition(n, P)
+    pl = sh.Plan.loopback(P, n, part, row_ptr, col, val, N, flags=sh.F_TRANSPOSE)
+    Bd = torch.from_numpy(B).cuda()
+    Cd = torch.full((n, N), float("nan"), device="cuda")
+    pl.spmm_loopback(Bd, Cd)
+    torch.cuda.synchronize()
+    trp, tcol, tval = csr_transpose(n, row_ptr, col, val)
+    assert np.array_equal(Cd.cpu().numpy().astype(np.float64), oracle.spmm_ref(trp, tcol, tval, B))
