@@ -239,14 +239,14 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
   while (cur < nrows) flush();              // last row and trailing empty rows
 }
 
-template <int LPR, int VPL, bool ACCUM, bool TWO, int MINB, int U, bool OUTP>
-__global__ void __launch_bounds__(kBlock, MINB) k_spmm(const SpmmArgs a) {
+template <int LPR, int VPL, bool ACCUM, bool TWO, int MINB, int U, bool OUTP, int BS = kBlock>
+__global__ void __launch_bounds__(BS, MINB) k_spmm(const SpmmArgs a) {
   constexpr int R = 32 / LPR;   // lane groups per warp
   const int lane = threadIdx.x & 31;
   const int sub = lane / LPR;
   const int li = lane % LPR;
   const unsigned mask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (sub * LPR));
-  const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const int64_t warp = ((int64_t)blockIdx.x * BS + threadIdx.x) >> 5;
   spmm_unit<LPR, VPL, ACCUM, TWO, (U < LPR ? U : LPR), OUTP>(a, warp * R + sub, li, mask);
 }
 
@@ -431,19 +431,20 @@ inline int64_t blocks_for(int64_t units, int rows_per_warp) {
   return (units + per_block - 1) / per_block;
 }
 
-template <int LPR, int VPL, int MINB, int U>
+template <int LPR, int VPL, int MINB, int U, int BS = kBlock>
 void spmm_launch(const SpmmArgs &a, bool acc, cudaStream_t s) {
   const int64_t units = a.n_tasks + a.n_groups;
-  const unsigned grid = (unsigned)blocks_for(units, 32 / LPR);
+  const int64_t per_block = (int64_t)(BS / 32) * (32 / LPR);
+  const unsigned grid = (unsigned)((units + per_block - 1) / per_block);
   const bool two = a.X1 != nullptr;
   if (a.out_ptr) {   // fused exchange: overwrite rows in peer buffers
-    k_spmm<LPR, VPL, false, false, MINB, U, true><<<grid, kBlock, 0, s>>>(a);
+    k_spmm<LPR, VPL, false, false, MINB, U, true, BS><<<grid, BS, 0, s>>>(a);
   } else if (acc) {
-    if (two) k_spmm<LPR, VPL, true, true, MINB, U, false><<<grid, kBlock, 0, s>>>(a);
-    else k_spmm<LPR, VPL, true, false, MINB, U, false><<<grid, kBlock, 0, s>>>(a);
+    if (two) k_spmm<LPR, VPL, true, true, MINB, U, false, BS><<<grid, BS, 0, s>>>(a);
+    else k_spmm<LPR, VPL, true, false, MINB, U, false, BS><<<grid, BS, 0, s>>>(a);
   } else {
-    if (two) k_spmm<LPR, VPL, false, true, MINB, U, false><<<grid, kBlock, 0, s>>>(a);
-    else k_spmm<LPR, VPL, false, false, MINB, U, false><<<grid, kBlock, 0, s>>>(a);
+    if (two) k_spmm<LPR, VPL, false, true, MINB, U, false, BS><<<grid, BS, 0, s>>>(a);
+    else k_spmm<LPR, VPL, false, false, MINB, U, false, BS><<<grid, BS, 0, s>>>(a);
   }
 }
 
@@ -453,7 +454,11 @@ int spmm_variant() {
   static int v = -1;
   if (v < 0) {
     const char *e = getenv("SHIRO_KVAR");
-    v = e ? atoi(e) : 4;
+    v = e ? atoi(e) : 0;
+    if (const char *k = getenv("SHIRO_KERNEL")) {   // 4, 11..18: CTA-size variants of k_spmm
+      const int kk = atoi(k);
+      if (kk >= 11 || kk == 4) v = kk;
+    }
   }
   return v;
 }
@@ -461,17 +466,36 @@ int spmm_variant() {
 template <int LPR, int VPL>
 void spmm_shape(const SpmmArgs &a, bool acc, cudaStream_t s) {
   if (VPL > 1) { spmm_launch<LPR, VPL, 1, 8>(a, acc, s); return; }
+#ifdef SHIRO_KERNEL_SWEEP   // tuning builds only (SHIRO_SWEEP=1 python -m ...build)
   switch (spmm_variant()) {
-    case 1: spmm_launch<LPR, VPL, 3, 8>(a, acc, s); break;
-    case 3: spmm_launch<LPR, VPL, 4, 4>(a, acc, s); break;
-    case 4: spmm_launch<LPR, VPL, 5, 4>(a, acc, s); break;
-    case 5: spmm_launch<LPR, VPL, 6, 4>(a, acc, s); break;
-    case 6: spmm_launch<LPR, VPL, 1, 8>(a, acc, s); break;
-    case 7: spmm_launch<LPR, VPL, 5, 8>(a, acc, s); break;
-    case 8: spmm_launch<LPR, VPL, 6, 8>(a, acc, s); break;
-    case 2: spmm_launch<LPR, VPL, 4, 8>(a, acc, s); break;
-    default: spmm_launch<LPR, VPL, 5, 4>(a, acc, s); break;   // measured best (c2/c3/c4)
+    case 1: spmm_launch<LPR, VPL, 3, 8>(a, acc, s); return;
+    case 3: spmm_launch<LPR, VPL, 4, 4>(a, acc, s); return;
+    case 5: spmm_launch<LPR, VPL, 6, 4>(a, acc, s); return;
+    case 6: spmm_launch<LPR, VPL, 1, 8>(a, acc, s); return;
+    case 7: spmm_launch<LPR, VPL, 5, 8>(a, acc, s); return;
+    case 8: spmm_launch<LPR, VPL, 6, 8>(a, acc, s); return;
+    case 2: spmm_launch<LPR, VPL, 4, 8>(a, acc, s); return;
+    default: break;
   }
+#endif
+  switch (spmm_variant()) {   // CTA-size variants
+    case 4: spmm_launch<LPR, VPL, 5, 4>(a, acc, s); return;          // 8-warp CTAs, 48 regs
+    case 11: spmm_launch<LPR, VPL, 20, 4, 64>(a, acc, s); return;
+    case 12: spmm_launch<LPR, VPL, 10, 4, 128>(a, acc, s); return;
+    case 13: spmm_launch<LPR, VPL, 16, 8, 64>(a, acc, s); return;
+    case 15: spmm_launch<LPR, VPL, 32, 8, 32>(a, acc, s); return;
+    case 16: spmm_launch<LPR, VPL, 16, 4, 64>(a, acc, s); return;
+    case 17: spmm_launch<LPR, VPL, 24, 8, 32>(a, acc, s); return;
+    case 18: spmm_launch<LPR, VPL, 24, 4, 32>(a, acc, s); return;
+    default: break;
+  }
+  // measured best (profiles/r1_kernel_sweep.txt): one-warp CTAs, 32 per SM
+  // (the per-SM CTA limit), 64 registers without spills.  A CTA retires as
+  // soon as its single unit is done, so power-law unit lengths no longer
+  // leave finished warps idle inside a CTA (8-warp CTAs: 42 % achieved vs
+  // 62 % theoretical occupancy on c2), and the spills of the 48-register
+  // build are gone: -17..19 % on c2/c3/c4.
+  spmm_launch<LPR, VPL, 32, 4, 32>(a, acc, s);
 }
 
 template <int LPR, int VPL>
@@ -654,6 +678,7 @@ int launch_spmm(const SpmmArgs &a, bool accumulate, cudaStream_t s) {
   int lpr, vpl;
   if (vec_shape(a.N, &lpr, &vpl)) {
     if (a.n_tasks + a.n_groups == 0) return 0;
+    if (vpl == 1 && launch_spmm2(a, accumulate, s)) return 1;   // pipelined kernel (spmm2.cu)
     SHIRO_DISPATCH(a.N, spmm_shape, a, accumulate, s);
   } else {
     const int64_t grid = blocks_for(a.nrows, 1);

@@ -47,6 +47,9 @@ struct SpmmArgs {
 // accumulate: false -> Y = A*X (overwrite, empty rows get zeros); true -> Y += A*X
 // returns the number of kernel launches issued (0 if nothing to do)
 int launch_spmm(const SpmmArgs &a, bool accumulate, cudaStream_t s);
+// software-pipelined variant for N in {32, 64, 128} (spmm2.cu); 0 = not
+// applicable (or SHIRO_KERNEL=1 selects the original k_spmm)
+int launch_spmm2(const SpmmArgs &a, bool accumulate, cudaStream_t s);
 
 // K4: Y[dst[i]] = X[src[i]] for i < n (gather B rows into the send buffer)
 int launch_pack(int64_t n, const int32_t *src, const int32_t *dst, const float *X, float *Y,
