@@ -178,6 +178,19 @@ int shiro_spmm(shiro_plan_t plan, const float *B_p, float *C_p, void *stream);
  * Pinned host memory gives full PCIe bandwidth. */
 int shiro_spmm_host(shiro_plan_t plan, const float *B_host, float *C_host, void *stream);
 
+/* A batch of nb independent SpMMs with the same plan (e.g. feature blocks or
+ * GNN layers), HOST buffers: item i reads B_host[i] ([M_p x N] fp32) and
+ * writes C_host[i] ([M_p x N] fp32).  Collective: every rank passes the same
+ * nb.  Uploads, SpMMs and downloads are pipelined over the batch (upload of
+ * item i overlaps the download of item i-1 on the full-duplex PCIe link; one
+ * device copy of B and C, owned by the plan).  `stream` orders the SpMMs;
+ * returns after every C_host[i] is written.  B_host/C_host are arrays of nb
+ * host pointers (pinned memory for full bandwidth); nb = 0 is a no-op.
+ * Errors: SHIRO_E_ARG (NULL arrays with nb > 0, negative nb, loopback or
+ * HOST_ONLY plan), SHIRO_E_CUDA. */
+int shiro_spmm_host_batch(shiro_plan_t plan, int64_t nb, const float *const *B_host,
+                          float *const *C_host, void *stream);
+
 /* Release the plan (local, not collective).  NULL is a no-op. */
 int shiro_free(shiro_plan_t plan);
 

@@ -91,6 +91,7 @@ def load():
         "shiro_plan": [ctypes.POINTER(DistT), I64, P, P, P, P, I32, P, ctypes.POINTER(P)],
         "shiro_spmm": [P, P, P, P],
         "shiro_spmm_host": [P, P, P, P],
+        "shiro_spmm_host_batch": [P, I64, P, P, P],
         "shiro_free": [P],
         "shiro_plan_info": [P, ctypes.POINTER(InfoT)],
         "shiro_plan_list": [P, I32, I32, P, I64, ctypes.POINTER(I64)],
@@ -211,6 +212,18 @@ class Plan:
         cp = C.ctypes.data if isinstance(C, np.ndarray) else C.data_ptr()
         _check(load().shiro_spmm_host(self._h, ctypes.c_void_p(bp), ctypes.c_void_p(cp),
                                       _stream_ptr(stream)))
+
+    def spmm_host_batch(self, Bs, Cs, stream=None):
+        """shiro_spmm_host_batch: item i reads host buffer Bs[i], writes Cs[i]
+        (uploads, SpMMs and downloads pipelined over the batch)."""
+        if len(Bs) != len(Cs):
+            raise ValueError("Bs and Cs differ in length")
+        ptr = lambda x: x.ctypes.data if isinstance(x, np.ndarray) else x.data_ptr()
+        nb = len(Bs)
+        bp = (ctypes.c_void_p * max(nb, 1))(*[ptr(b) for b in Bs])
+        cp = (ctypes.c_void_p * max(nb, 1))(*[ptr(c) for c in Cs])
+        _check(load().shiro_spmm_host_batch(self._h, nb, ctypes.cast(bp, ctypes.c_void_p),
+                                            ctypes.cast(cp, ctypes.c_void_p), _stream_ptr(stream)))
 
     def spmm_loopback(self, B, C, stream=None):
         _check(load().shiro_spmm_loopback(self._h, ctypes.c_void_p(B.data_ptr()),

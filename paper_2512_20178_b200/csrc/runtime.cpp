@@ -33,6 +33,10 @@ Plan::~Plan() {
     if (comm_stream) cudaStreamDestroy(comm_stream);
     if (arena) cudaFree(arena);
     if (stage) cudaFree(stage);
+    for (cudaEvent_t e : {ev_in, ev_comp, ev_out})
+      if (e) cudaEventDestroy(e);
+    if (h2d_s) cudaStreamDestroy(h2d_s);
+    if (d2h_s) cudaStreamDestroy(d2h_s);
     for (auto &e : prof)
       if (e) cudaEventDestroy(e);
   }
@@ -1141,6 +1145,50 @@ int shiro_spmm_host(shiro_plan_t plan, const float *B_host, float *C_host, void 
     if (bytes) SHIRO_CK(cudaMemcpyAsync(C_host, dC, bytes, cudaMemcpyDeviceToHost, s));
     SHIRO_CK(cudaStreamSynchronize(s));
     plan->last_launches = pl.last_launches;
+  });
+}
+
+int shiro_spmm_host_batch(shiro_plan_t plan, int64_t nb, const float *const *B_host,
+                          float *const *C_host, void *stream) {
+  return guarded([&] {
+    if (!plan || plan->loopback || plan->view) throw Error(SHIRO_E_ARG, "not a distributed plan");
+    if (nb < 0 || (nb > 0 && (!B_host || !C_host))) throw Error(SHIRO_E_ARG, "bad batch");
+    Plan &pl = *plan->single;
+    if (!pl.arena) throw Error(SHIRO_E_ARG, "plan was built with SHIRO_F_HOST_ONLY");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t bytes = (size_t)pl.M * pl.N * sizeof(float);
+    if (!pl.stage && bytes) SHIRO_CK(cudaMalloc(&pl.stage, 2 * bytes));
+    if (!pl.h2d_s) {
+      SHIRO_CK(cudaStreamCreateWithFlags(&pl.h2d_s, cudaStreamNonBlocking));
+      SHIRO_CK(cudaStreamCreateWithFlags(&pl.d2h_s, cudaStreamNonBlocking));
+      for (cudaEvent_t *e : {&pl.ev_in, &pl.ev_comp, &pl.ev_out})
+        SHIRO_CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
+    float *dB = pl.stage, *dC = pl.stage ? pl.stage + (size_t)pl.M * pl.N : nullptr;
+    // Pipeline over the batch with one device copy of B and C: the upload of
+    // B[i] waits only for SpMM i-1 to finish reading dB, and overlaps the
+    // download of C[i-1] (PCIe is full duplex); SpMM i waits for its upload
+    // and for the download of C[i-1] to finish reading dC.  Steady state per
+    // item: max(H2D, D2H) + the SpMM.
+    SHIRO_CK(cudaEventRecord(pl.ev_comp, s));
+    SHIRO_CK(cudaEventRecord(pl.ev_out, s));
+    int64_t launches = 0;
+    for (int64_t i = 0; i < nb; ++i) {
+      SHIRO_CK(cudaStreamWaitEvent(pl.h2d_s, pl.ev_comp, 0));
+      if (bytes) SHIRO_CK(cudaMemcpyAsync(dB, B_host[i], bytes, cudaMemcpyHostToDevice, pl.h2d_s));
+      SHIRO_CK(cudaEventRecord(pl.ev_in, pl.h2d_s));
+      SHIRO_CK(cudaStreamWaitEvent(s, pl.ev_in, 0));
+      SHIRO_CK(cudaStreamWaitEvent(s, pl.ev_out, 0));
+      exec_plan(pl, dB, dC, s);
+      launches += pl.last_launches;
+      SHIRO_CK(cudaEventRecord(pl.ev_comp, s));
+      SHIRO_CK(cudaStreamWaitEvent(pl.d2h_s, pl.ev_comp, 0));
+      if (bytes) SHIRO_CK(cudaMemcpyAsync(C_host[i], dC, bytes, cudaMemcpyDeviceToHost, pl.d2h_s));
+      SHIRO_CK(cudaEventRecord(pl.ev_out, pl.d2h_s));
+    }
+    SHIRO_CK(cudaStreamWaitEvent(s, pl.ev_out, 0));
+    SHIRO_CK(cudaStreamSynchronize(s));
+    plan->last_launches = launches;
   });
 }
 

@@ -181,8 +181,10 @@ struct Plan {
   cudaStream_t g_s = nullptr;
   bool g_prof = false;
   int64_t g_launches = 0;
-  // device staging of B and C for shiro_spmm_host
+  // device staging of B and C for shiro_spmm_host / shiro_spmm_host_batch
   float *stage = nullptr;
+  cudaStream_t h2d_s = nullptr, d2h_s = nullptr;   // copy engines of the batch pipeline
+  cudaEvent_t ev_in = nullptr, ev_comp = nullptr, ev_out = nullptr;
 
   ~Plan();
 };

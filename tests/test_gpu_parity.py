@@ -183,6 +183,22 @@ def test_host_buffers_e2e():
     assert ok, info
 
 
+def test_host_batch_pipelined():
+    """shiro_spmm_host_batch: distinct B per item, each C exact (integer mode),
+    and the pipeline must not mix items (upload i vs download i-1)."""
+    c = shiro_gen.CONFIGS["c1"]
+    row_ptr, col, vi = shiro_gen.gen_matrix("c1", value_mode=1)
+    pl = sh.Plan.distributed(0, 1, c.n, np.array([0, c.n]), row_ptr, col, vi, c.N)
+    Bs = [torch.from_numpy(np.asarray(shiro_gen.gen_B(c.seed + i, 0, c.n, c.N, mode=1))).pin_memory()
+          for i in range(5)]
+    Cs = [torch.full((c.n, c.N), float("nan")).pin_memory() for _ in range(5)]
+    pl.spmm_host_batch(Bs, Cs)
+    for B, C in zip(Bs, Cs):
+        assert np.array_equal(C.numpy().astype(np.float64),
+                              oracle.spmm_ref(row_ptr, col, vi, B.numpy()))
+    pl.spmm_host_batch([], [])
+
+
 def test_profile_stage_times():
     c = shiro_gen.CONFIGS["c1"]
     row_ptr, col, val = shiro_gen.gen_matrix("c1")
