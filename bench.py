@@ -350,7 +350,19 @@ def main():
     # max over ranks, per step and per stage
     t = torch.tensor(step_ms, dtype=torch.float64, device=dev)
     st = torch.tensor([[s[x] for x in sh.STAGES] for s in stages], dtype=torch.float64, device=dev)
+    per_rank = None
     if world > 1:
+        mine = st.mean(0)
+        allr = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(allr, mine)
+        per_rank = [{k: round(v, 4) for k, v in zip(sh.STAGES, r.cpu().numpy().tolist()) if v}
+                    for r in allr]
+        wk = torch.tensor([float(info["op_nnz"][op]) for op in sh.OPS], dtype=torch.float64,
+                          device=dev)
+        allw = [torch.empty_like(wk) for _ in range(world)]
+        dist.all_gather(allw, wk)
+        for d_, w_ in zip(per_rank, allw):
+            d_["op_nnz"] = {op: int(x) for op, x in zip(sh.OPS, w_.cpu().numpy().tolist()) if x}
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(st, op=dist.ReduceOp.MAX)
     step_ms = t.cpu().numpy()
@@ -484,6 +496,7 @@ def main():
             "exchange": exch,
             "gather_probe": gather,
             "stages_ms": {k: round(v, 5) for k, v in stage_ms.items()},
+            "stages_ms_per_rank": per_rank,
             "step_ms": {"median": round(float(np.median(step_ms)), 5),
                         "p10": round(float(np.percentile(step_ms, 10)), 5),
                         "p90": round(float(np.percentile(step_ms, 90)), 5)},

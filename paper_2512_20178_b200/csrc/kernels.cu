@@ -56,6 +56,30 @@ __device__ __forceinline__ void add4(float4 &acc, const float4 &x) {
   acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
 }
 
+// Early READY of the fused exchange (SpmmArgs::sig_*): called by a whole lane
+// group after its peer-destined unit is stored.  Every lane fences its own
+// NVLink stores at system scope before lane 0 counts the unit; the lane group
+// that counts the last unit fences again (fence-fence synchronisation through
+// the counter) and publishes READY with release semantics.
+__device__ __noinline__ void sig_unit_done(int32_t *ctr, int32_t target, const int32_t *epoch,
+                                          int32_t *const *ptrs, int32_t n, int li, unsigned mask) {
+  __threadfence_system();
+  __syncwarp(mask);
+  if (li == 0) {
+    const int d = atomicAdd(ctr, 1);
+    if (d == target - 1) {
+      __threadfence_system();
+      const int32_t v = *epoch + 1;
+      for (int i = 0; i < n; ++i)
+        asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(ptrs[i]), "r"(v) : "memory");
+      *ctr = 0;   // re-arm for the next launch
+    }
+  }
+  __syncwarp(mask);
+}
+#define SHIRO_SIG_DONE(a, li, mask) \
+  sig_unit_done((a).sig_ctr, (a).sig_target, (a).sig_epoch, (a).sig_ptrs, (a).sig_n, li, mask)
+
 // Output row address of a pointer-routed row: a peer (or own) buffer address,
 // or -- top bit set -- a row index into Y (the caller's C: local rows of the
 // fused producer launch, whose address is only known at call time).
@@ -168,6 +192,7 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
         y[li + q * LPR] = s[q];
       }
       if (li == 0) a.long_counter[lr] = 0;    // re-arm for the next launch
+      if (OUTP && a.sig_ptrs && t < a.sig_rows) SHIRO_SIG_DONE(a, li, mask);
     }
     return;
   }
@@ -237,6 +262,7 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
     }
   }
   while (cur < nrows) flush();              // last row and trailing empty rows
+  if (OUTP && a.sig_ptrs && g.r0 < a.sig_rows) SHIRO_SIG_DONE(a, li, mask);
 }
 
 template <int LPR, int VPL, bool ACCUM, bool TWO, int MINB, int U, bool OUTP, int BS = kBlock>

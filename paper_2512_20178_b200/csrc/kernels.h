@@ -42,6 +42,17 @@ struct SpmmArgs {
   const int32_t *long_first = nullptr;  // [n_long+1] first task of each long row
   int32_t *long_counter = nullptr;      // [n_long] zero-initialised arrival counters
   float *scratch = nullptr;             // [n_tasks * N] chunk partials
+  // Early READY (fused exchange producer): rows [0, sig_rows) go to peers.
+  // When the last of their sig_target units (row groups + hub rows) has been
+  // stored, the lane group finishing it raises READY = *sig_epoch + 1 at the
+  // sig_n peer flags sig_ptrs[] (after system-scope fences), while the
+  // launch's local rows are still being computed.  sig_ptrs == nullptr: off.
+  int64_t sig_rows = 0;
+  int32_t sig_target = 0;
+  int32_t sig_n = 0;
+  int32_t *sig_ctr = nullptr;           // zero-initialised, re-armed by the signaller
+  int32_t *const *sig_ptrs = nullptr;
+  const int32_t *sig_epoch = nullptr;
 };
 
 // accumulate: false -> Y = A*X (overwrite, empty rows get zeros); true -> Y += A*X

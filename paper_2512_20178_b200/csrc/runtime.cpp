@@ -72,11 +72,11 @@ size_t put(Arena &ar, const std::vector<T> &v) {
 // that they still spread over ~64 lane groups per SM (one lane group walks
 // its unit serially, ~1 memory round trip per U = 8 gathers, so the unit
 // length bounds the latency of small, latency-bound ops).
-constexpr int32_t kChunk = 256, kChunkMin = 32;
+constexpr int32_t kChunk = 256, kChunkMin = 64;   // one-warp CTAs: c2 best at 64 (32: +7 %)
 
 int32_t unit_size(int64_t nnz) {
   if (const char *e = getenv("SHIRO_CHUNK")) return std::max(kChunkMin, atoi(e));
-  int64_t L = nnz / ((int64_t)num_sms() * 128);   // c2: 64 (swept 32..256), c3/c4: 256
+  int64_t L = nnz / ((int64_t)num_sms() * 128);   // c2: 64 (swept 32..128), c3/c4: 256 (swept 128..1024)
   L = (L / 32) * 32;
   return (int32_t)std::max<int64_t>(kChunkMin, std::min<int64_t>(kChunk, L));
 }
@@ -122,7 +122,8 @@ SplitHost make_split(const HostCsr &c, int N) {
     }
     const int64_t r0 = t;
     int64_t sum = 0;
-    while (t < c.nrows && deg(t) <= s.L && t - r0 < max_rows && (t == r0 || sum + deg(t) <= s.L)) {
+    while (t < c.nrows && deg(t) <= s.L && t - r0 < max_rows && (t == r0 || sum + deg(t) <= s.L) &&
+           (t == r0 || t != c.split_row)) {
       for (int64_t k = c.rp[t]; k < c.rp[t + 1]; ++k) s.roff[k] = (uint8_t)(t - r0);
       sum += deg(t);
       ++t;
@@ -298,9 +299,11 @@ void upload_prod(Plan &pl, const std::vector<int32_t> &pack_src,
     outp.push_back((1ull << 63) | (uint64_t)t);       // local row of C
   }
   c.nrows = (int64_t)outp.size();
+  c.split_row = np + pl.A_out.nrows;   // peer-destined rows first (early READY)
   Arena ar;
   SpmmLayout L = layout_spmm(ar, c, pl.N);
   const size_t o_ptr = put(ar, outp);
+  const size_t o_sig = ar.reserve(sizeof(int32_t));   // zeroed early-READY counter
   SHIRO_CK(cudaMalloc(&pl.prod_ops, std::max<size_t>(ar.total, 256)));
   SHIRO_CK(cudaMemset(pl.prod_ops, 0, std::max<size_t>(ar.total, 256)));
   char *base = static_cast<char *>(pl.prod_ops);
@@ -309,6 +312,12 @@ void upload_prod(Plan &pl, const std::vector<int32_t> &pack_src,
       SHIRO_CK(cudaMemcpy(base + it.off, it.src, it.bytes, cudaMemcpyHostToDevice));
   pl.d_prod = bind_spmm(base, L, c, pl.N);
   pl.d_prod.a.out_ptr = reinterpret_cast<float *const *>(base + o_ptr);
+  pl.d_prod.a.sig_rows = c.split_row;
+  pl.d_prod.a.sig_ctr = reinterpret_cast<int32_t *>(base + o_sig);
+  int32_t target = 0;
+  for (const RowGroup &g : L.sp.groups) target += (g.r0 < c.split_row) ? 1 : 0;
+  for (int32_t r : L.sp.long_row) target += (r < c.split_row) ? 1 : 0;
+  pl.d_prod.a.sig_target = target;
   pl.info.dev_bytes += (int64_t)ar.total;
   // the fused launch is the "local" op of a step; pack/partial fold into it
   std::vector<int32_t> src(c.col);
@@ -569,6 +578,21 @@ bool fused_step_enabled() {
   return v == 1;
 }
 
+// SHIRO_EARLY_READY=1: the producer raises READY from inside its launch once
+// the peer-destined units are stored.  Opt-in: measured slower at P=2 (c4
+// 1.66 vs 1.55 ms, c3 2.81 vs 2.67 ms, profiles/r1_early_ready_P2.txt): the
+// system-scope fence each peer-destined unit needs before it is counted
+// stalls its warp for an NVLink round trip, which costs more than the
+// separate k_signal launch it saves.
+bool early_ready_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("SHIRO_EARLY_READY");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
   if (*pl.err_host) throw Error(SHIRO_E_PEER, "fused exchange: a peer did not signal in time");
   auto rec = [&](int i) {
@@ -609,9 +633,19 @@ void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
       return;
     }
   }
-  launches += run_spmm(pl.d_prod, B, pl.M, nullptr, C, false, s);
+  // producer: peer-destined rows first; the lane group storing the last of
+  // them raises READY at the peers from inside the launch (early READY), so
+  // the exchange drains while the local rows are computed
+  DevSpmm prod = pl.d_prod;
+  const bool early = early_ready_enabled() && prod.a.sig_target > 0 && P > 1;
+  if (early) {
+    prod.a.sig_ptrs = pl.ready_ptrs;
+    prod.a.sig_n = P - 1;
+    prod.a.sig_epoch = ep;
+  }
+  launches += run_spmm(prod, B, pl.M, nullptr, C, false, s);
   rec(6);
-  launches += launch_signal(pl.ready_ptrs, P - 1, ep, 1, false, s);
+  if (!early) launches += launch_signal(pl.ready_ptrs, P - 1, ep, 1, false, s);
   rec(3);
   launches += launch_wait(pl.xflags, P, ep, 1, err, pl.wait_timeout_ns, s);
   rec(4);

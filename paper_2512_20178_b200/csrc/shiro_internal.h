@@ -48,6 +48,7 @@ struct HostCsr {
   std::vector<float> val;       // empty = all ones
   std::vector<int32_t> out_row;
   bool ptr_rows = false;        // rows addressed by per-row output pointers
+  int64_t split_row = -1;       // row groups never straddle this row (early READY)
   int64_t nnz() const { return (int64_t)col.size(); }
 };
 
