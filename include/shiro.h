@@ -242,6 +242,15 @@ int shiro_stage_times(shiro_plan_t plan, double *ms /* [SHIRO_NUM_STAGES] */);
 int shiro_probe_gather(const float *X, int32_t N, const int32_t *idx, int64_t n_idx, float *out,
                        int32_t chunk, void *stream);
 
+/* TMA variant of the probe (measurement only): the same sums with the rows
+ * staged into shared memory by cp.async.bulk.tensor tile::gather4 (4 rows per
+ * instruction) through a `stages`-deep ring per warp (stages in {2, 4, 8}).
+ * X: device [x_rows x N] fp32, N = 128 only; chunk a multiple of 4.
+ * Errors: SHIRO_E_ARG (shape), SHIRO_E_CUDA (no tensor-map entry point,
+ * launch failure). */
+int shiro_probe_gather_tma(const float *X, int64_t x_rows, int32_t N, const int32_t *idx,
+                           int64_t n_idx, float *out, int32_t chunk, int32_t stages, void *stream);
+
 /* Number of kernel launches the last shiro_spmm* issued on this plan (all
  * virtual ranks for loopback), NCCL kernels excluded. */
 int64_t shiro_last_launches(shiro_plan_t plan);

@@ -101,6 +101,7 @@ def load():
         "shiro_profile": [P, I32],
         "shiro_stage_times": [P, P],
         "shiro_probe_gather": [P, I32, P, I64, P, I32, P],
+        "shiro_probe_gather_tma": [P, I64, I32, P, I64, P, I32, I32, P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -137,6 +138,14 @@ def probe_gather(X, idx, out, chunk=256, stream=None):
     _check(load().shiro_probe_gather(ctypes.c_void_p(X.data_ptr()), X.shape[1],
                                      ctypes.c_void_p(idx.data_ptr()), idx.numel(),
                                      ctypes.c_void_p(out.data_ptr()), chunk, _stream_ptr(stream)))
+
+
+def probe_gather_tma(X, idx, out, chunk=256, stages=4, stream=None):
+    """shiro_probe_gather_tma (TMA gather4 staging) on torch CUDA tensors."""
+    _check(load().shiro_probe_gather_tma(ctypes.c_void_p(X.data_ptr()), X.shape[0], X.shape[1],
+                                         ctypes.c_void_p(idx.data_ptr()), idx.numel(),
+                                         ctypes.c_void_p(out.data_ptr()), chunk, stages,
+                                         _stream_ptr(stream)))
 
 
 def get_unique_id() -> bytes:

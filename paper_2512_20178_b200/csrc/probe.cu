@@ -4,6 +4,8 @@
 // an SpMM's own column-index stream it times the unavoidable part of that
 // SpMM -- every referenced source row delivered to an SM once per nonzero --
 // which is the gather-aware roofline of DESIGN.md section 5.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -44,7 +46,125 @@ __global__ void __launch_bounds__(256) k_probe_gather(const float *__restrict__ 
   reinterpret_cast<float4 *>(out + c * N)[li] = acc;
 }
 
+// ---- TMA variant: the same sum, rows staged by cp.async.bulk.tensor
+// tile::gather4 (4 rows of 512 B per instruction) into an S-stage shared
+// memory ring per warp (one warp per CTA); lane 0 issues, every lane reads
+// its float4 of each staged row.  In-flight bytes cost shared memory instead
+// of registers.  N = 128 only (box = 128 fp32 x 1 row, 4 rows per gather4).
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_gather4(void *dst, const CUtensorMap *tm, uint64_t *bar, int r0,
+                                            int r1, int r2, int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(smem_u32(bar)), "r"(0), "r"(r0), "r"(r1), "r"(r2),
+      "r"(r3)
+      : "memory");
+}
+
+template <int S>
+__global__ void __launch_bounds__(32) k_probe_gather_tma(const __grid_constant__ CUtensorMap tm,
+                                                         const int32_t *__restrict__ idx, int64_t n,
+                                                         int chunk, float *__restrict__ out) {
+  extern __shared__ __align__(128) float4 ring[];   // S x 4 rows x 32 float4
+  __shared__ __align__(8) uint64_t bar[S];
+  const int li = threadIdx.x;
+  const int64_t kb = (int64_t)blockIdx.x * chunk;
+  const int64_t ke = (kb + chunk < n) ? kb + chunk : n;
+  const int cnt = (int)(ke - kb);
+  const int nq = (cnt + 3) / 4;
+  if (li == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  auto issue = [&](int q) {   // lane 0 only
+    const int s = q % S;
+    int r[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) r[i] = __ldg(idx + kb + ((4 * q + i < cnt) ? 4 * q + i : 0));
+    mbar_expect_tx(&bar[s], 4 * 512);
+    tma_gather4(ring + s * 128, &tm, &bar[s], r[0], r[1], r[2], r[3]);
+  };
+  if (li == 0)
+    for (int q = 0; q < S && q < nq; ++q) issue(q);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int q = 0; q < nq; ++q) {
+    const int s = q % S;
+    mbar_wait(&bar[s], (uint32_t)((q / S) & 1));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (4 * q + i < cnt) {
+        const float4 x = ring[s * 128 + i * 32 + li];
+        acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+      }
+    }
+    __syncwarp();
+    if (li == 0 && q + S < nq) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads -> async writes
+      issue(q + S);
+    }
+  }
+  reinterpret_cast<float4 *>(out + blockIdx.x * 128LL)[li] = acc;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void *p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
 }  // namespace
+
+extern "C" int shiro_probe_gather_tma(const float *X, int64_t x_rows, int32_t N, const int32_t *idx,
+                                      int64_t n_idx, float *out, int32_t chunk, int32_t stages,
+                                      void *stream) {
+  if (!X || !idx || !out || n_idx < 0 || chunk < 4 || chunk % 4 || N != 128 || x_rows < 1)
+    return SHIRO_E_ARG;
+  if (stages != 2 && stages != 4 && stages != 8) return SHIRO_E_ARG;
+  auto enc = encode_fn();
+  if (!enc) return SHIRO_E_CUDA;
+  CUtensorMap tm;
+  const cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)x_rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)N * sizeof(float)};
+  const cuuint32_t box[2] = {(cuuint32_t)N, 1};
+  const cuuint32_t estr[2] = {1, 1};
+  if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(X), dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return SHIRO_E_CUDA;
+  const int64_t grid = (n_idx + chunk - 1) / chunk;
+  if (grid == 0) return SHIRO_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t smem = (size_t)stages * 4 * 512;
+  if (stages == 2) k_probe_gather_tma<2><<<(unsigned)grid, 32, smem, s>>>(tm, idx, n_idx, chunk, out);
+  else if (stages == 4) k_probe_gather_tma<4><<<(unsigned)grid, 32, smem, s>>>(tm, idx, n_idx, chunk, out);
+  else k_probe_gather_tma<8><<<(unsigned)grid, 32, smem, s>>>(tm, idx, n_idx, chunk, out);
+  return cudaGetLastError() == cudaSuccess ? SHIRO_OK : SHIRO_E_CUDA;
+}
 
 extern "C" int shiro_probe_gather(const float *X, int32_t N, const int32_t *idx, int64_t n_idx,
                                   float *out, int32_t chunk, void *stream) {
