@@ -40,6 +40,45 @@ __device__ __forceinline__ int2 ld_stream_cv(const int2 *p) {
                : "l"(p));
   return v;
 }
+// L2 eviction-policy variants (HINT, SHIRO_L2HINT): 0 = default policies;
+// 1 = the streams read or written once (A's (col, val) pairs, C rows) are
+// L2 evict_first; 2 = 1 + the gathered B rows evict_last.
+__device__ __forceinline__ uint64_t pol_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t pol_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+template <int HINT>
+__device__ __forceinline__ int2 ldcv_h(const int2 *p) {
+  if (HINT == 0) return ld_stream_cv(p);
+  int2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;"
+               : "=r"(v.x), "=r"(v.y)
+               : "l"(p), "l"(pol_first()));
+  return v;
+}
+template <int HINT>
+__device__ __forceinline__ float4 ldB_h(const float4 *p) {
+  if (HINT < 2) return __ldg(p);
+  float4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p), "l"(pol_last()));
+  return v;
+}
+template <int HINT>
+__device__ __forceinline__ void stY_h(float4 *p, const float4 &v) {
+  if (HINT == 0) { *p = v; return; }
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol_first())
+               : "memory");
+}
+
 __device__ __forceinline__ int ld_stream_u8(const uint8_t *p) {
   unsigned short v;
   asm volatile("ld.global.nc.L1::no_allocate.u8 %0, [%1];" : "=h"(v) : "l"(p));
@@ -97,7 +136,7 @@ __device__ __forceinline__ const float4 *src_row(const SpmmArgs &a, int c) {
 
 // Gather U source rows for nonzeros j..j+U-1 of the current batch; the
 // weights are broadcast together with the columns, before any FMA.
-template <int LPR, int VPL, bool TWO, int U>
+template <int LPR, int VPL, bool TWO, int U, int HINT = 0>
 __device__ __forceinline__ void gather(const SpmmArgs &a, float4 (&x)[U][VPL], float (&w)[U],
                                        int c, float v, int j, int cnt, int li, unsigned mask) {
 #pragma unroll
@@ -107,7 +146,7 @@ __device__ __forceinline__ void gather(const SpmmArgs &a, float4 (&x)[U][VPL], f
     if (j + u < cnt) {               // uniform across the lane group
       const float4 *r = src_row<TWO>(a, cu);
 #pragma unroll
-      for (int q = 0; q < VPL; ++q) x[u][q] = __ldg(r + li + q * LPR);
+      for (int q = 0; q < VPL; ++q) x[u][q] = ldB_h<HINT>(r + li + q * LPR);
       w[u] = vu;
     } else {
 #pragma unroll
@@ -120,7 +159,7 @@ __device__ __forceinline__ void gather(const SpmmArgs &a, float4 (&x)[U][VPL], f
 // One work unit u: a chunk task (u < n_tasks) or a row group.  OUTP: output
 // rows are addressed by a per-row pointer (e.g. a peer's receive buffer over
 // NVLink, the fused exchange) instead of Y + out_row * N.
-template <int LPR, int VPL, bool ACCUM, bool TWO, int U, bool OUTP>
+template <int LPR, int VPL, bool ACCUM, bool TWO, int U, bool OUTP, int HINT = 0>
 __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, const int li,
                                           const unsigned mask) {
   float4 acc[VPL];
@@ -139,12 +178,12 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
     for (int64_t base = kb; base < ke; base += LPR) {
       const int64_t k = base + li;
       int2 cv = make_int2(0, 0);
-      if (k < ke) cv = ld_stream_cv(a.cv + k);
+      if (k < ke) cv = ldcv_h<HINT>(a.cv + k);
       const int cnt = (int)((ke - base) < LPR ? (ke - base) : LPR);
       for (int j = 0; j < cnt; j += U) {
         float4 x[U][VPL];
         float w[U];
-        gather<LPR, VPL, TWO, U>(a, x, w, cv.x, __int_as_float(cv.y), j, cnt, li, mask);
+        gather<LPR, VPL, TWO, U, HINT>(a, x, w, cv.x, __int_as_float(cv.y), j, cnt, li, mask);
 #pragma unroll
         for (int uu = 0; uu < U; ++uu)
 #pragma unroll
@@ -232,7 +271,7 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
 #pragma unroll
     for (int q = 0; q < VPL; ++q) {
       if (ACCUM) add4(acc[q], y[li + q * LPR]);
-      y[li + q * LPR] = acc[q];
+      stY_h<HINT>(y + li + q * LPR, acc[q]);
       acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     ++cur;
@@ -242,14 +281,14 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
     int2 cv = make_int2(0, 0);
     int ro = 0;
     if (k < g.k1) {
-      cv = ld_stream_cv(a.cv + k);
+      cv = ldcv_h<HINT>(a.cv + k);
       ro = ld_stream_u8(a.roff + k);
     }
     const int cnt = (int)((g.k1 - base) < LPR ? (g.k1 - base) : LPR);
     for (int j = 0; j < cnt; j += U) {
       float4 x[U][VPL];
       float w[U];
-      gather<LPR, VPL, TWO, U>(a, x, w, cv.x, __int_as_float(cv.y), j, cnt, li, mask);
+      gather<LPR, VPL, TWO, U, HINT>(a, x, w, cv.x, __int_as_float(cv.y), j, cnt, li, mask);
 #pragma unroll
       for (int uu = 0; uu < U; ++uu) {
         const int rou = __shfl_sync(mask, ro, j + uu, LPR);
@@ -265,7 +304,8 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
   if (OUTP && a.sig_ptrs && g.r0 < a.sig_rows) SHIRO_SIG_DONE(a, li, mask);
 }
 
-template <int LPR, int VPL, bool ACCUM, bool TWO, int MINB, int U, bool OUTP, int BS = kBlock>
+template <int LPR, int VPL, bool ACCUM, bool TWO, int MINB, int U, bool OUTP, int BS = kBlock,
+          int HINT = 0>
 __global__ void __launch_bounds__(BS, MINB) k_spmm(const SpmmArgs a) {
   constexpr int R = 32 / LPR;   // lane groups per warp
   const int lane = threadIdx.x & 31;
@@ -273,7 +313,7 @@ __global__ void __launch_bounds__(BS, MINB) k_spmm(const SpmmArgs a) {
   const int li = lane % LPR;
   const unsigned mask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (sub * LPR));
   const int64_t warp = ((int64_t)blockIdx.x * BS + threadIdx.x) >> 5;
-  spmm_unit<LPR, VPL, ACCUM, TWO, (U < LPR ? U : LPR), OUTP>(a, warp * R + sub, li, mask);
+  spmm_unit<LPR, VPL, ACCUM, TWO, (U < LPR ? U : LPR), OUTP, HINT>(a, warp * R + sub, li, mask);
 }
 
 // Generic width (N not a supported vector width): one warp per CSR row,
@@ -457,20 +497,20 @@ inline int64_t blocks_for(int64_t units, int rows_per_warp) {
   return (units + per_block - 1) / per_block;
 }
 
-template <int LPR, int VPL, int MINB, int U, int BS = kBlock>
+template <int LPR, int VPL, int MINB, int U, int BS = kBlock, int H = 0>
 void spmm_launch(const SpmmArgs &a, bool acc, cudaStream_t s) {
   const int64_t units = a.n_tasks + a.n_groups;
   const int64_t per_block = (int64_t)(BS / 32) * (32 / LPR);
   const unsigned grid = (unsigned)((units + per_block - 1) / per_block);
   const bool two = a.X1 != nullptr;
   if (a.out_ptr) {   // fused exchange: overwrite rows in peer buffers
-    k_spmm<LPR, VPL, false, false, MINB, U, true, BS><<<grid, BS, 0, s>>>(a);
+    k_spmm<LPR, VPL, false, false, MINB, U, true, BS, H><<<grid, BS, 0, s>>>(a);
   } else if (acc) {
-    if (two) k_spmm<LPR, VPL, true, true, MINB, U, false, BS><<<grid, BS, 0, s>>>(a);
-    else k_spmm<LPR, VPL, true, false, MINB, U, false, BS><<<grid, BS, 0, s>>>(a);
+    if (two) k_spmm<LPR, VPL, true, true, MINB, U, false, BS, H><<<grid, BS, 0, s>>>(a);
+    else k_spmm<LPR, VPL, true, false, MINB, U, false, BS, H><<<grid, BS, 0, s>>>(a);
   } else {
-    if (two) k_spmm<LPR, VPL, false, true, MINB, U, false, BS><<<grid, BS, 0, s>>>(a);
-    else k_spmm<LPR, VPL, false, false, MINB, U, false, BS><<<grid, BS, 0, s>>>(a);
+    if (two) k_spmm<LPR, VPL, false, true, MINB, U, false, BS, H><<<grid, BS, 0, s>>>(a);
+    else k_spmm<LPR, VPL, false, false, MINB, U, false, BS, H><<<grid, BS, 0, s>>>(a);
   }
 }
 
@@ -521,6 +561,9 @@ void spmm_shape(const SpmmArgs &a, bool acc, cudaStream_t s) {
   // leave finished warps idle inside a CTA (8-warp CTAs: 42 % achieved vs
   // 62 % theoretical occupancy on c2), and the spills of the 48-register
   // build are gone: -17..19 % on c2/c3/c4.
+  static const int hint = getenv("SHIRO_L2HINT") ? atoi(getenv("SHIRO_L2HINT")) : 0;
+  if (LPR == 32 && VPL == 1 && hint == 1) { spmm_launch<LPR, VPL, 32, 4, 32, 1>(a, acc, s); return; }
+  if (LPR == 32 && VPL == 1 && hint == 2) { spmm_launch<LPR, VPL, 32, 4, 32, 2>(a, acc, s); return; }
   spmm_launch<LPR, VPL, 32, 4, 32>(a, acc, s);
 }
 

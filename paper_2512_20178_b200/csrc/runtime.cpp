@@ -68,17 +68,24 @@ size_t put(Arena &ar, const std::vector<T> &v) {
 // nonzeros and kMaxGroupRows rows (2*LPR when an out_row map is used),
 // streamed by one lane group; a per-nonzero byte holds the row offset inside
 // the group.
-// Unit size L: 256 nonzeros for large ops; small ops use smaller units so
-// that they still spread over ~64 lane groups per SM (one lane group walks
-// its unit serially, ~1 memory round trip per U = 8 gathers, so the unit
-// length bounds the latency of small, latency-bound ops).
-constexpr int32_t kChunk = 256, kChunkMin = 64;   // one-warp CTAs: c2 best at 64 (32: +7 %)
+// Unit size L: 256 nonzeros for large ops; smaller ops use smaller units so
+// that the launch still has ~W waves of one-warp CTAs (32 per SM).  A lane
+// group walks its unit serially, ~1 memory round trip per U = 4 gathers, so
+// when an op fits in about one wave its time is the longest unit's chain of
+// round trips: small ops (the remote SpMM and the per-rank producers of c2 at
+// P >= 2) need short units.  L = nnz / (SMs * 32 * W), W = 4 (SHIRO_WAVES),
+// rounded down to a multiple of 8, clamped to [8, 256] (SHIRO_CHUNK_MIN /
+// SHIRO_CHUNK override; c2 at P = 1 lands at 56-64, c3/c4 at 256).
+constexpr int32_t kChunk = 256;
 
 int32_t unit_size(int64_t nnz) {
-  if (const char *e = getenv("SHIRO_CHUNK")) return std::max(kChunkMin, atoi(e));
-  int64_t L = nnz / ((int64_t)num_sms() * 128);   // c2: 64 (swept 32..128), c3/c4: 256 (swept 128..1024)
-  L = (L / 32) * 32;
-  return (int32_t)std::max<int64_t>(kChunkMin, std::min<int64_t>(kChunk, L));
+  static const int32_t fixed = getenv("SHIRO_CHUNK") ? atoi(getenv("SHIRO_CHUNK")) : 0;
+  static const int32_t lmin = getenv("SHIRO_CHUNK_MIN") ? std::max(1, atoi(getenv("SHIRO_CHUNK_MIN"))) : 8;
+  static const int32_t waves = getenv("SHIRO_WAVES") ? std::max(1, atoi(getenv("SHIRO_WAVES"))) : 4;
+  if (fixed > 0) return fixed;
+  int64_t L = nnz / ((int64_t)num_sms() * 32 * waves);
+  L = (L / 8) * 8;
+  return (int32_t)std::max<int64_t>(lmin, std::min<int64_t>(kChunk, L));
 }
 constexpr int32_t kMaxGroupRows = 64;
 
@@ -106,14 +113,18 @@ SplitHost make_split(const HostCsr &c, int N) {
   const int64_t max_rows = (c.out_row.empty() && !c.ptr_rows) ? kMaxGroupRows
                                                               : std::min(kMaxGroupRows, 2 * lpr);
   auto deg = [&](int64_t r) { return c.rp[r + 1] - c.rp[r]; };
+  // hub threshold: rows longer than H become chunk tasks; a row of L < deg <= H
+  // is a unit of its own (no chunk reduction for moderately long rows)
+  static const int64_t hmin = getenv("SHIRO_HUB_MIN") ? atoi(getenv("SHIRO_HUB_MIN")) : 64;
+  const int64_t H = std::max<int64_t>(s.L, hmin);
   int64_t t = 0;
   while (t < c.nrows) {
-    if (deg(t) > s.L) {
+    if (deg(t) > H) {
       const int32_t lr = (int32_t)s.long_row.size();
       s.long_row.push_back((int32_t)t);
-      // chunk length ~max(L, sqrt(deg)): balances the serial walk of one chunk
+      // chunk length ~max(H, sqrt(deg)): balances the serial walk of one chunk
       // against the in-order reduction of the chunk partials (both ~latency-bound)
-      const int64_t clen = std::max<int64_t>(s.L, (int64_t)std::sqrt((double)deg(t)));
+      const int64_t clen = std::max<int64_t>(H, (int64_t)std::sqrt((double)deg(t)));
       const int64_t nch = (deg(t) + clen - 1) / clen;
       for (int64_t k = 0; k < nch; ++k) s.task_long.push_back(lr);
       s.long_first.push_back((int32_t)s.task_long.size());
@@ -122,7 +133,7 @@ SplitHost make_split(const HostCsr &c, int N) {
     }
     const int64_t r0 = t;
     int64_t sum = 0;
-    while (t < c.nrows && deg(t) <= s.L && t - r0 < max_rows && (t == r0 || sum + deg(t) <= s.L) &&
+    while (t < c.nrows && deg(t) <= H && t - r0 < max_rows && (t == r0 || sum + deg(t) <= s.L) &&
            (t == r0 || t != c.split_row)) {
       for (int64_t k = c.rp[t]; k < c.rp[t + 1]; ++k) s.roff[k] = (uint8_t)(t - r0);
       sum += deg(t);
