@@ -108,8 +108,12 @@ typedef struct {
                          (contiguous, must divide nranks)                        */
   uint32_t flags;     /* SHIRO_F_*                                              */
   const void *nccl_id; /* 128-byte ncclUniqueId from shiro_get_unique_id on rank
-                         0, identical on all ranks; NULL iff nranks == 1 or
-                         (SHIRO_F_HOST_ONLY and host_xchg != NULL)               */
+                         0, identical on all ranks; may be NULL if
+                         nranks == 1, or if host_xchg != NULL and either
+                         SHIRO_F_HOST_ONLY is set or the fused NVLink
+                         exchange is used (no NCCL communicator is created;
+                         shiro_plan fails with SHIRO_E_ARG on every rank if
+                         the peer mappings cannot be set up)              */
   shiro_alltoallv_fn host_xchg; /* optional plan-time transport (e.g. gloo);
                                    NULL = use NCCL                              */
   void *host_xchg_ctx;

@@ -561,7 +561,13 @@ void spmm_shape(const SpmmArgs &a, bool acc, cudaStream_t s) {
   // leave finished warps idle inside a CTA (8-warp CTAs: 42 % achieved vs
   // 62 % theoretical occupancy on c2), and the spills of the 48-register
   // build are gone: -17..19 % on c2/c3/c4.
-  static const int hint = getenv("SHIRO_L2HINT") ? atoi(getenv("SHIRO_L2HINT")) : 0;
+  // L2 policy (profiles/r1_kernel_sweep.txt, "L2 hints"): when the source
+  // rows fit comfortably in L2 (c2: 87 MB) the streams (A, C) go evict_first
+  // and the gathered rows evict_last (c2 -5 %); for sources far larger than
+  // L2 (c3/c4) the hints measured neutral to +0.5 %, so none.
+  static const int env_hint = getenv("SHIRO_L2HINT") ? atoi(getenv("SHIRO_L2HINT")) : -1;
+  const int hint = env_hint >= 0 ? env_hint
+                                 : ((a.X1 == nullptr && a.n0 * (int64_t)a.N * 4 <= (96ll << 20)) ? 2 : 0);
   if (LPR == 32 && VPL == 1 && hint == 1) { spmm_launch<LPR, VPL, 32, 4, 32, 1>(a, acc, s); return; }
   if (LPR == 32 && VPL == 1 && hint == 2) { spmm_launch<LPR, VPL, 32, 4, 32, 2>(a, acc, s); return; }
   spmm_launch<LPR, VPL, 32, 4, 32>(a, acc, s);

@@ -93,8 +93,8 @@ int launch_pack_ptr(int64_t n, const int32_t *src, float *const *dstp, const flo
 // *err = 1 and gives up instead of hanging the GPU.
 int launch_signal(int32_t *const *flags, int n, int32_t *epoch, int add, bool bump,
                   cudaStream_t s);
-int launch_wait(const int32_t *flags, int n, const int32_t *epoch, int add, int32_t *err,
-                int64_t timeout_ns, cudaStream_t s);
+int launch_wait(const int32_t *flags, int n, int32_t *epoch, int add, int32_t *err,
+                int64_t timeout_ns, cudaStream_t s, bool bump = false);   // bump: *epoch = value after the wait
 
 // K5: C[tgt[u]] += sum_{k in [ptr[u], ptr[u+1])} R[src[k]] (gather-sum of
 // received partial C rows, fixed order: C first, then sources ascending)

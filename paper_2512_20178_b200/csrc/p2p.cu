@@ -45,8 +45,8 @@ __global__ void k_signal(int32_t *const *flags, int n, int32_t *epoch, int add, 
   }
 }
 
-__global__ void k_wait(const int32_t *flags, int n, const int32_t *epoch, int add, int32_t *err,
-                       int64_t timeout_ns) {
+__global__ void k_wait(const int32_t *flags, int n, int32_t *epoch, int add, int32_t *err,
+                       int64_t timeout_ns, int bump) {
   const int i = threadIdx.x;
   const int32_t value = *epoch + add;
   if (i < n) {
@@ -61,6 +61,7 @@ __global__ void k_wait(const int32_t *flags, int n, const int32_t *epoch, int ad
   }
   __syncthreads();
   __threadfence_system();
+  if (bump && i == 0) *epoch = value;   // every thread has read the epoch before the barrier
 }
 
 }  // namespace
@@ -72,10 +73,10 @@ int launch_signal(int32_t *const *flags, int n, int32_t *epoch, int add, bool bu
   return 1;
 }
 
-int launch_wait(const int32_t *flags, int n, const int32_t *epoch, int add, int32_t *err,
-                int64_t timeout_ns, cudaStream_t s) {
+int launch_wait(const int32_t *flags, int n, int32_t *epoch, int add, int32_t *err,
+                int64_t timeout_ns, cudaStream_t s, bool bump) {
   if (n <= 0) return 0;
-  k_wait<<<1, 64, 0, s>>>(flags, n, epoch, add, err, timeout_ns);
+  k_wait<<<1, 64, 0, s>>>(flags, n, epoch, add, err, timeout_ns, bump ? 1 : 0);
   return 1;
 }
 

@@ -20,7 +20,7 @@ namespace {
 
 struct PeerMsg {
   cudaIpcMemHandle_t handle;
-  int64_t recv_buf_off, flags_off, recv_row_off;
+  int64_t recv_buf_off, flags_off, recv_row_off, recv_buf2_off;
 };
 
 template <typename T>
@@ -53,7 +53,7 @@ void p2p_setup(Plan &pl, const Alltoallv &xchg) {
   int status = cudaIpcGetMemHandle(&h, pl.arena) == cudaSuccess ? 0 : 1;
   std::vector<std::vector<char>> send(P), recv;
   for (int d = 0; d < P; ++d) {
-    PeerMsg m{h, pl.recv_buf_off, pl.flags_off, pl.recv_off[d]};
+    PeerMsg m{h, pl.recv_buf_off, pl.flags_off, pl.recv_off[d], pl.recv_buf2_off};
     send[d] = bytes_of(m);
   }
   xchg(send, recv);
@@ -90,22 +90,40 @@ void p2p_setup(Plan &pl, const Alltoallv &xchg) {
   auto peer_recv = [&](int d) {
     return reinterpret_cast<char *>(pl.peer_base[d]) + pm[d].recv_buf_off;
   };
-  std::vector<uint64_t> dstp, outp, rdy, cons;
+  // double buffering needs a second receive buffer on every rank (and not the
+  // opt-in single-launch step, which keeps the CONSUMED protocol)
+  bool dbuf = pl.recv_buf2_off >= 0;
+  for (int d = 0; d < P; ++d)
+    if (d != me && pm[d].recv_buf2_off < 0) dbuf = false;
+  if (const char *e = getenv("SHIRO_FUSED_STEP"))
+    if (e[0] == '1') dbuf = false;
+  std::vector<uint64_t> dstp, outp, dstp2, outp2, rdy, cons;
   for (int d = 0; d < P; ++d) {
     if (d == me) continue;
     char *base = peer_recv(d) + pm[d].recv_row_off * rowb;
-    for (size_t k = 0; k < pl.send_b[d].size(); ++k)
+    char *base2 = dbuf ? reinterpret_cast<char *>(pl.peer_base[d]) + pm[d].recv_buf2_off +
+                             pm[d].recv_row_off * rowb
+                       : nullptr;
+    for (size_t k = 0; k < pl.send_b[d].size(); ++k) {
       dstp.push_back((uint64_t)(base + (int64_t)k * rowb));
+      if (dbuf) dstp2.push_back((uint64_t)(base2 + (int64_t)k * rowb));
+    }
     const int64_t nb = (int64_t)pl.send_b[d].size();
-    for (size_t k = 0; k < pl.send_c[d].size(); ++k)
+    for (size_t k = 0; k < pl.send_c[d].size(); ++k) {
       outp.push_back((uint64_t)(base + (nb + (int64_t)k) * rowb));
+      if (dbuf) outp2.push_back((uint64_t)(base2 + (nb + (int64_t)k) * rowb));
+    }
     char *fl = reinterpret_cast<char *>(pl.peer_base[d]) + pm[d].flags_off;
     rdy.push_back((uint64_t)(fl + sizeof(int32_t) * me));
     cons.push_back((uint64_t)(fl + sizeof(int32_t) * (P + me)));
   }
   if ((int64_t)outp.size() != pl.d_out.a.nrows || (int64_t)dstp.size() != pl.d_pack.n)
     throw Error(SHIRO_E_INTERNAL, "fused exchange: row count mismatch");
-  upload_prod(pl, pl.pack_src, dstp, outp);   // K4 + K3 + K1 as one pointer-routed launch
+  // K4 + K3 + K1 as one pointer-routed launch (one destination table per buffer)
+  if (dbuf) upload_prod(pl, pl.pack_src, dstp, outp, &dstp2, &outp2);
+  else upload_prod(pl, pl.pack_src, dstp, outp);
+  pl.dbuf = dbuf;
+  pl.step_parity = 0;
   const size_t n_all = rdy.size() + cons.size();
   // pointer arrays, then 2 x uint64 of fused-step work counters
   SHIRO_CK(cudaMalloc(&pl.p2p_arena, (n_all + 2) * sizeof(uint64_t)));

@@ -24,7 +24,8 @@ namespace shiro {
 
 Plan::~Plan() {
   if (!loopback_view) {
-    if (graph) cudaGraphExecDestroy(graph);
+    for (auto &g : graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
     p2p_release(*this);
     hier_release(*this);
     if (comm) ncclCommDestroy(comm);
@@ -191,12 +192,25 @@ DevSpmm bind_spmm(char *base, const SpmmLayout &L, const HostCsr &c, int N) {
 
 }  // namespace
 
+// SHIRO_DBUF=0 keeps one receive buffer and the CONSUMED round trip
+bool dbuf_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("SHIRO_DBUF");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 void plan_upload(Plan &pl, cudaStream_t s) {
   SHIRO_CK(cudaGetDevice(&pl.device));
   Arena ar;
   const int N = pl.N;
   const size_t o_send = ar.reserve((size_t)pl.send_rows * N * sizeof(float));
   const size_t o_recv = ar.reserve((size_t)pl.recv_rows * N * sizeof(float));
+  // second receive buffer for the double-buffered fused exchange
+  const bool want2 = pl.P > 1 && !(pl.flags & SHIRO_F_XCHG_NCCL) && dbuf_enabled();
+  const size_t o_recv2 = want2 ? ar.reserve((size_t)pl.recv_rows * N * sizeof(float)) : 0;
   // fused-exchange flags: ready[P], consumed[P], err (IPC-exported with the arena)
   const size_t o_flags = ar.reserve((2 * (size_t)pl.P + 2) * sizeof(int32_t));
   const bool fused = !(pl.flags & SHIRO_F_SPLIT_RECV);
@@ -219,6 +233,10 @@ void plan_upload(Plan &pl, cudaStream_t s) {
   pl.recv_buf = reinterpret_cast<float *>(base + o_recv);
   pl.xflags = reinterpret_cast<int32_t *>(base + o_flags);
   pl.recv_buf_off = (int64_t)o_recv;
+  if (want2) {
+    pl.recv_buf2 = reinterpret_cast<float *>(base + o_recv2);
+    pl.recv_buf2_off = (int64_t)o_recv2;
+  }
   pl.flags_off = (int64_t)o_flags;
   pl.d_diag = bind_spmm(base, l_diag, pl.A_diag, N);
   pl.d_out = bind_spmm(base, l_out, pl.A_out, N);
@@ -281,10 +299,12 @@ void plan_drop_host(Plan &pl) {
 static bool prod_ops_exist(const Plan &pl) { return pl.prod_ops != nullptr; }
 
 void upload_prod(Plan &pl, const std::vector<int32_t> &pack_src,
-                 const std::vector<uint64_t> &pack_addr, const std::vector<uint64_t> &part_addr) {
+                 const std::vector<uint64_t> &pack_addr, const std::vector<uint64_t> &part_addr,
+                 const std::vector<uint64_t> *pack_addr2, const std::vector<uint64_t> *part_addr2) {
   HostCsr c;
   c.ptr_rows = true;
-  std::vector<uint64_t> outp;
+  std::vector<uint64_t> outp, outp2;
+  const bool two = pack_addr2 && part_addr2;
   const int64_t np = (int64_t)pack_src.size();
   if (prod_ops_exist(pl)) { cudaFree(pl.prod_ops); pl.prod_ops = nullptr; }
   for (int64_t i = 0; i < np; ++i) {
@@ -292,6 +312,7 @@ void upload_prod(Plan &pl, const std::vector<int32_t> &pack_src,
     c.val.push_back(1.0f);
     c.rp.push_back((int64_t)c.col.size());
     outp.push_back(pack_addr[i]);
+    if (two) outp2.push_back((*pack_addr2)[i]);
   }
   for (int64_t t = 0; t < pl.A_out.nrows; ++t) {
     for (int64_t k = pl.A_out.rp[t]; k < pl.A_out.rp[t + 1]; ++k) {
@@ -300,6 +321,7 @@ void upload_prod(Plan &pl, const std::vector<int32_t> &pack_src,
     }
     c.rp.push_back((int64_t)c.col.size());
     outp.push_back(part_addr[t]);
+    if (two) outp2.push_back((*part_addr2)[t]);
   }
   for (int64_t t = 0; t < pl.A_diag.nrows; ++t) {
     for (int64_t k = pl.A_diag.rp[t]; k < pl.A_diag.rp[t + 1]; ++k) {
@@ -308,12 +330,14 @@ void upload_prod(Plan &pl, const std::vector<int32_t> &pack_src,
     }
     c.rp.push_back((int64_t)c.col.size());
     outp.push_back((1ull << 63) | (uint64_t)t);       // local row of C
+    if (two) outp2.push_back((1ull << 63) | (uint64_t)t);
   }
   c.nrows = (int64_t)outp.size();
   c.split_row = np + pl.A_out.nrows;   // peer-destined rows first (early READY)
   Arena ar;
   SpmmLayout L = layout_spmm(ar, c, pl.N);
   const size_t o_ptr = put(ar, outp);
+  const size_t o_ptr2 = two ? put(ar, outp2) : 0;
   const size_t o_sig = ar.reserve(sizeof(int32_t));   // zeroed early-READY counter
   SHIRO_CK(cudaMalloc(&pl.prod_ops, std::max<size_t>(ar.total, 256)));
   SHIRO_CK(cudaMemset(pl.prod_ops, 0, std::max<size_t>(ar.total, 256)));
@@ -323,6 +347,8 @@ void upload_prod(Plan &pl, const std::vector<int32_t> &pack_src,
       SHIRO_CK(cudaMemcpy(base + it.off, it.src, it.bytes, cudaMemcpyHostToDevice));
   pl.d_prod = bind_spmm(base, L, c, pl.N);
   pl.d_prod.a.out_ptr = reinterpret_cast<float *const *>(base + o_ptr);
+  pl.prod_out_ptr[0] = pl.d_prod.a.out_ptr;
+  pl.prod_out_ptr[1] = two ? reinterpret_cast<float *const *>(base + o_ptr2) : nullptr;
   pl.d_prod.a.sig_rows = c.split_row;
   pl.d_prod.a.sig_ctr = reinterpret_cast<int32_t *>(base + o_sig);
   int32_t target = 0;
@@ -612,6 +638,39 @@ void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
   const int P = pl.P;
   int32_t *err = pl.xflags + 2 * P, *ep = pl.xflags + 2 * P + 1;  // device epoch e-1
   int64_t launches = 0;
+  if (pl.dbuf) {
+    // Double-buffered: step e's rows land in the peers' buffer e mod 2.  A
+    // peer read that buffer last in its remote SpMM of step e-2, which
+    // precedes (stream order) its producer and READY of step e-1, which this
+    // rank waited for before this producer: no CONSUMED wait or signal.
+    //   producer (peer buffer e%2) -> READY = e -> wait READY >= e (sets the
+    //   epoch) -> remote SpMM over my buffer e%2
+    const int par = pl.step_parity;
+    float *rb = par ? pl.recv_buf2 : pl.recv_buf;
+    rec(0); rec(1); rec(2); rec(5);
+    DevSpmm prod = pl.d_prod;
+    prod.a.out_ptr = pl.prod_out_ptr[par];
+    launches += run_spmm(prod, B, pl.M, nullptr, C, false, s);
+    rec(6);
+    launches += launch_signal(pl.ready_ptrs, P - 1, ep, 1, false, s);
+    rec(3);
+    launches += launch_wait(pl.xflags, P, ep, 1, err, pl.wait_timeout_ns, s, true);
+    rec(4);
+    if (!(pl.flags & SHIRO_F_SPLIT_RECV)) {
+      launches += run_spmm(pl.d_rem, rb, pl.recv_rows, nullptr, C, true, s);
+      rec(7);
+    } else {
+      launches += run_spmm(pl.d_col, rb, pl.recv_rows, nullptr, C, true, s);
+      rec(7);
+      launches += launch_scatter_add(pl.d_scatter.nt, pl.d_scatter.tgt, pl.d_scatter.ptr,
+                                     pl.d_scatter.src, rb, C, pl.N, s);
+    }
+    rec(8);
+    SHIRO_CK(cudaMemcpyAsync(pl.err_host, err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    pl.last_launches = launches;
+    pl.prof_used = 3;
+    return;
+  }
   rec(0);
   launches += launch_wait(pl.xflags + P, P, ep, 0, err, pl.wait_timeout_ns, s);
   rec(1);
@@ -722,32 +781,41 @@ bool graph_eligible(const Plan &pl, cudaStream_t s) {
 void launch_graph(Plan &pl, const float *B, float *C, cudaStream_t s) {
   if (pl.err_host && *pl.err_host)
     throw Error(SHIRO_E_PEER, "fused exchange: a peer did not signal in time");
-  if (!pl.graph || pl.g_B != B || pl.g_C != C || pl.g_s != s || pl.g_prof != pl.prof_on) {
-    if (pl.graph) {
-      cudaGraphExecDestroy(pl.graph);
-      pl.graph = nullptr;
+  Plan::GraphSlot &g = pl.graphs[pl.dbuf ? pl.step_parity : 0];
+  if (!g.exec || g.B != B || g.C != C || g.s != s || g.prof != pl.prof_on) {
+    if (g.exec) {
+      cudaGraphExecDestroy(g.exec);
+      g.exec = nullptr;
     }
     SHIRO_CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    cudaGraph_t g = nullptr;
+    cudaGraph_t cg = nullptr;
     try {
       exec_plan(pl, B, C, s);
     } catch (...) {
-      cudaStreamEndCapture(s, &g);
-      if (g) cudaGraphDestroy(g);
+      cudaStreamEndCapture(s, &cg);
+      if (cg) cudaGraphDestroy(cg);
       throw;
     }
-    SHIRO_CK(cudaStreamEndCapture(s, &g));
-    const cudaError_t ie = cudaGraphInstantiate(&pl.graph, g, 0);
-    cudaGraphDestroy(g);
+    SHIRO_CK(cudaStreamEndCapture(s, &cg));
+    const cudaError_t ie = cudaGraphInstantiate(&g.exec, cg, 0);
+    cudaGraphDestroy(cg);
     SHIRO_CK(ie);
-    pl.g_B = B;
-    pl.g_C = C;
-    pl.g_s = s;
-    pl.g_prof = pl.prof_on;
-    pl.g_launches = pl.last_launches;
+    g.B = B;
+    g.C = C;
+    g.s = s;
+    g.prof = pl.prof_on;
+    g.launches = pl.last_launches;
   }
-  SHIRO_CK(cudaGraphLaunch(pl.graph, s));
-  pl.last_launches = pl.g_launches;
+  SHIRO_CK(cudaGraphLaunch(g.exec, s));
+  pl.last_launches = g.launches;
+}
+
+// One step through the graph or direct launches; advances the step parity
+// of the double-buffered exchange (every rank calls in the same order).
+void run_step(Plan &pl, const float *B, float *C, cudaStream_t s) {
+  if (graph_eligible(pl, s)) launch_graph(pl, B, C, s);
+  else exec_plan(pl, B, C, s);
+  if (pl.dbuf) pl.step_parity ^= 1;
 }
 
 int fail(const Error &e) {
@@ -916,7 +984,12 @@ int shiro_plan(const shiro_dist_t *d, int64_t n, const int64_t *part, const int6
           callback_alltoallv(d->host_xchg, d->host_xchg_ctx, d->nranks, d->rank, snd, rcv);
         };
       }
-      if (!host_only || !d->host_xchg) {
+      // NCCL communicator: needed for the NCCL exchange or as the plan-time
+      // transport; skipped when a host transport is given and the fused
+      // exchange (IPC peer stores, no NCCL) carries the data
+      const bool need_nccl = !d->host_xchg || (d->flags & SHIRO_F_XCHG_NCCL) ||
+                             (!host_only && d->nccl_id);
+      if (need_nccl) {
         if (!d->nccl_id) throw Error(SHIRO_E_ARG, "nccl_id is NULL with nranks > 1");
         ncclUniqueId id;
         std::memcpy(&id, d->nccl_id, 128);
@@ -988,7 +1061,9 @@ int shiro_plan(const shiro_dist_t *d, int64_t n, const int64_t *part, const int6
         hier_upload(pl);
         hier_p2p_setup(pl, xchg);
       } else if (d->nranks > 1 && !(d->flags & SHIRO_F_XCHG_NCCL)) {
-        p2p_setup(pl, xchg);
+        p2p_setup(pl, xchg);   // collective: every rank agrees on p2p or not
+        if (!pl.p2p && !pl.comm)
+          throw Error(SHIRO_E_ARG, "fused exchange unavailable and no nccl_id for the NCCL exchange");
       }
       plan_drop_host(pl);
     }
@@ -1166,11 +1241,7 @@ int shiro_spmm(shiro_plan_t plan, const float *B_p, float *C_p, void *stream) {
         throw Error(SHIRO_E_NCCL, std::string("asynchronous NCCL error: ") + ncclGetErrorString(as));
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (graph_eligible(pl, s)) {
-      launch_graph(pl, B_p, C_p, s);
-    } else {
-      exec_plan(pl, B_p, C_p, s);
-    }
+    run_step(pl, B_p, C_p, s);
     SHIRO_CK(cudaGetLastError());
     plan->last_launches = pl.last_launches;
   });
@@ -1186,7 +1257,7 @@ int shiro_spmm_host(shiro_plan_t plan, const float *B_host, float *C_host, void 
     if (!pl.stage && bytes) SHIRO_CK(cudaMalloc(&pl.stage, 2 * bytes));   // once per plan
     float *dB = pl.stage, *dC = pl.stage ? pl.stage + (size_t)pl.M * pl.N : nullptr;
     if (bytes) SHIRO_CK(cudaMemcpyAsync(dB, B_host, bytes, cudaMemcpyHostToDevice, s));
-    exec_plan(pl, dB, dC, s);
+    run_step(pl, dB, dC, s);
     if (bytes) SHIRO_CK(cudaMemcpyAsync(C_host, dC, bytes, cudaMemcpyDeviceToHost, s));
     SHIRO_CK(cudaStreamSynchronize(s));
     plan->last_launches = pl.last_launches;
@@ -1224,7 +1295,7 @@ int shiro_spmm_host_batch(shiro_plan_t plan, int64_t nb, const float *const *B_h
       SHIRO_CK(cudaEventRecord(pl.ev_in, pl.h2d_s));
       SHIRO_CK(cudaStreamWaitEvent(s, pl.ev_in, 0));
       SHIRO_CK(cudaStreamWaitEvent(s, pl.ev_out, 0));
-      exec_plan(pl, dB, dC, s);
+      run_step(pl, dB, dC, s);
       launches += pl.last_launches;
       SHIRO_CK(cudaEventRecord(pl.ev_comp, s));
       SHIRO_CK(cudaStreamWaitEvent(pl.d2h_s, pl.ev_comp, 0));

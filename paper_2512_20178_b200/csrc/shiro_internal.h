@@ -148,6 +148,7 @@ struct Plan {
   void *arena = nullptr;
   size_t arena_bytes = 0;
   float *send_buf = nullptr, *recv_buf = nullptr;
+  float *recv_buf2 = nullptr;         // second receive buffer (double-buffered fused exchange)
   DevSpmm d_diag, d_out, d_col, d_rem;
   DevPack d_pack;
   DevScatter d_scatter;
@@ -163,7 +164,12 @@ struct Plan {
   bool p2p = false;
   int32_t epoch = 0;
   int32_t *xflags = nullptr;          // local: ready[P], consumed[P], err
-  int64_t recv_buf_off = 0, flags_off = 0;
+  int64_t recv_buf_off = 0, flags_off = 0, recv_buf2_off = -1;
+  // double buffering: step parity selects the receive buffer peers write
+  // (and the producer's destination table); no CONSUMED round trip
+  bool dbuf = false;
+  int step_parity = 0;
+  float *const *prod_out_ptr[2] = {nullptr, nullptr};
   std::vector<void *> peer_base;      // opened IPC mappings
   void *p2p_arena = nullptr;
   int32_t *const *ready_ptrs = nullptr, *const *consumed_ptrs = nullptr;
@@ -176,12 +182,14 @@ struct Plan {
   int64_t wait_timeout_ns = 20000000000LL;
   // CUDA graph of one step (P = 1, fused exchange, hierarchical), keyed by
   // (B, C, stream, profiling); replayed while the key matches
-  cudaGraphExec_t graph = nullptr;
-  const float *g_B = nullptr;
-  float *g_C = nullptr;
-  cudaStream_t g_s = nullptr;
-  bool g_prof = false;
-  int64_t g_launches = 0;
+  struct GraphSlot {
+    cudaGraphExec_t exec = nullptr;
+    const float *B = nullptr;
+    float *C = nullptr;
+    cudaStream_t s = nullptr;
+    bool prof = false;
+    int64_t launches = 0;
+  } graphs[2];                        // one per step parity (double buffering)
   // device staging of B and C for shiro_spmm_host / shiro_spmm_host_batch
   float *stage = nullptr;
   cudaStream_t h2d_s = nullptr, d2h_s = nullptr;   // copy engines of the batch pipeline
@@ -239,10 +247,13 @@ void p2p_setup(Plan &plan, const Alltoallv &xchg);
 // build + upload the fused producer op; pack_addr / part_addr are the
 // destination addresses of the packed B rows and of the A_out rows
 void upload_prod(Plan &plan, const std::vector<int32_t> &pack_src,
-                 const std::vector<uint64_t> &pack_addr, const std::vector<uint64_t> &part_addr);
+                 const std::vector<uint64_t> &pack_addr, const std::vector<uint64_t> &part_addr,
+                 const std::vector<uint64_t> *pack_addr2 = nullptr,
+                 const std::vector<uint64_t> *part_addr2 = nullptr);
 void plan_drop_host(Plan &plan);
 void p2p_release(Plan &plan);
 void exec_p2p(Plan &plan, const float *B, float *C, cudaStream_t s);
+bool dbuf_enabled();   // SHIRO_DBUF (default on): double-buffered fused exchange
 void exec_plan(Plan &plan, const float *B, float *C, cudaStream_t s);
 
 }  // namespace shiro
