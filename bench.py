@@ -248,6 +248,7 @@ def main():
     ap.add_argument("--group-size", type=int, default=1)
     ap.add_argument("--split-recv", action="store_true", help="SHIRO_F_SPLIT_RECV (K2 and K5 as two launches)")
     ap.add_argument("--colmax", action="store_true", help="SHIRO_F_COVER_COLMAX")
+    ap.add_argument("--balance", action="store_true", help="SHIRO_F_COVER_BALANCE (R18)")
     ap.add_argument("--mode", default="joint", choices=["joint", "col", "row"])
     ap.add_argument("--xchg", default="p2p", choices=["p2p", "nccl"],
                     help="fused NVLink exchange (default) or NCCL grouped send/recv")
@@ -293,6 +294,8 @@ def main():
         flags |= sh.F_SPLIT_RECV
     if args.colmax:
         flags |= sh.F_COVER_COLMAX
+    if args.balance:
+        flags |= sh.F_COVER_BALANCE
     flags |= {"joint": 0, "col": sh.F_MODE_COL, "row": sh.F_MODE_ROW}[args.mode]
     if args.xchg == "nccl":
         flags |= sh.F_XCHG_NCCL
@@ -475,7 +478,8 @@ def main():
             "config": {"workload": f"{cfg.name}: {cfg.desc}", "n": cfg.n, "nnz": nnz, "N": cfg.N,
                        "P": world, "group_size": args.group_size,
                        "plan": ("split-recv " if args.split_recv else "") + args.mode +
-                               (" col-max" if args.colmax else " row-max"),
+                               (" col-max" if args.colmax else " row-max") +
+                               (" balanced (R18)" if args.balance else ""),
                        "partition": "uniform 1D rows (larger blocks first)",
                        "l2": "flushed (256 MiB memset) before every timed step",
                        "exchange": (args.xchg if world > 1 else "none"),

@@ -70,6 +70,12 @@ enum shiro_status {
 #define SHIRO_F_NO_OVERLAP (1u << 5)   /* local SpMM after the exchange (ablation)*/
 #define SHIRO_F_MODE_BLOCK (1u << 7)   /* sparsity-oblivious: whole B row block
                                           per non-empty A^(p,q) (Eq. 1) */
+#define SHIRO_F_COVER_BALANCE (1u << 9) /* joint mode: a block whose all-rows
+                                           cover is within max(1, mu/1000) rows
+                                           of the minimum mu is covered by all
+                                           its rows (column owner computes it),
+                                           balancing dense-ish blocks across
+                                           ranks (R18)               */
 #define SHIRO_F_TRANSPOSE (1u << 8)    /* plan and run A^T (GNN backward, SURVEY
                                           8(f) N3): the caller still passes its
                                           rows of A; one distributed transpose at

@@ -217,7 +217,12 @@ def _row_ids(row_ptr):
     return np.repeat(np.arange(row_ptr.size - 1, dtype=np.int64), np.diff(row_ptr))
 
 
-def plan_flat(n, part, row_ptr, col, mode="joint", rule="rowmax") -> FlatPlan:
+def balance_slack(mu):
+    """Row slack of the balanced cover rule: max(1, floor(mu / 1000)) (R18)."""
+    return max(1, int(mu) // 1000)
+
+
+def plan_flat(n, part, row_ptr, col, mode="joint", rule="rowmax", balance=False) -> FlatPlan:
     """Per ordered pair (p, q), p != q, decide per nonzero ROW vs COL.
 
     joint: canonical min cover of A^(p,q) (R1); nonzero (i,j) is
@@ -227,6 +232,11 @@ def plan_flat(n, part, row_ptr, col, mode="joint", rule="rowmax") -> FlatPlan:
     row:   every off-diagonal nonzero ROW (Eq. 3).
     block: sparsity-oblivious, q sends its whole B row block to every p with
            a non-empty A^(p,q) (Eq. 1); all nonzeros COL.
+    balance (joint only, R18, not from the paper): when the block's
+      all-rows cover is within balance_slack(mu) rows of the minimum mu, every
+      nonzero of the block is ROW (the column owner q computes the block), so
+      dense-ish symmetric blocks are computed by alternating sides instead of
+      all on one rank; bytes rise by at most the slack per block.
     Lists: send_b[(q,p)] = selected cols, send_c[(q,p)] = selected rows,
     global ids ascending."""
     part = np.asarray(part, np.int64)
@@ -261,6 +271,8 @@ def plan_flat(n, part, row_ptr, col, mode="joint", rule="rowmax") -> FlatPlan:
                 else:
                     is_row = ~np.isin(bj, sel_c)
                 assert sel_r.size + sel_c.size == mu
+                if balance and rows_u.size <= mu + balance_slack(mu):
+                    is_row = np.ones(idx.size, bool)
             elif mode == "col":
                 is_row = np.zeros(idx.size, bool)
             elif mode == "row":
@@ -545,7 +557,7 @@ def exec_hier(plan: FlatPlan, msgs, g, row_ptr, col, val, B):
 __all__ = [
     "ROW", "COL", "LOCAL", "build_oracle_lib", "uniform_partition", "owner_of",
     "spmm_ref", "min_cover_local", "min_cover", "brute_force_cover",
-    "max_matching_kuhn", "FlatPlan", "plan_flat", "volumes", "Msg", "rep_col",
+    "max_matching_kuhn", "FlatPlan", "balance_slack", "plan_flat", "volumes", "Msg", "rep_col",
     "rep_row", "plan_hier", "tier_traffic", "flat_inter_rows", "exec_flat",
     "exec_hier",
 ]

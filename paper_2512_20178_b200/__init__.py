@@ -5,7 +5,7 @@ The product is ``libshiro.so`` (C ABI, ``include/shiro.h``): host planner
 sources (``csrc/``), the in-tree build (``build.py``) and a thin ctypes
 binding (``binding.py``).  Nothing here imports ``oracle/``.
 """
-from .binding import (F_COVER_COLMAX, F_COVER_ROWMAX, F_SPLIT_RECV, F_HOST_ONLY, F_TRANSPOSE,  # noqa: F401
+from .binding import (F_COVER_COLMAX, F_COVER_ROWMAX, F_COVER_BALANCE, F_SPLIT_RECV, F_HOST_ONLY, F_TRANSPOSE,  # noqa: F401
                       F_MODE_BLOCK, F_MODE_COL, F_MODE_JOINT, F_MODE_ROW, F_NO_OVERLAP, F_XCHG_NCCL, LIST_RECV_B,
                       LIST_RECV_C, LIST_SEND_B, LIST_SEND_C, LIST_H1_SEND, LIST_H2_SEND,
                       LIST_H1_RECV, LIST_H2_RECV, Plan, ShiroError, get_unique_id, load,

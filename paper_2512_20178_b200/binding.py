@@ -26,6 +26,7 @@ F_MODE_JOINT = 0
 F_MODE_COL = 1 << 1
 F_MODE_ROW = 1 << 2
 F_SPLIT_RECV = 1 << 3
+F_COVER_BALANCE = 1 << 9
 F_HOST_ONLY = 1 << 4
 F_NO_OVERLAP = 1 << 5
 F_XCHG_NCCL = 1 << 6

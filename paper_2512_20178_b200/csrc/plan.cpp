@@ -178,6 +178,14 @@ Phase1 plan_phase1(const PlanInput &in) {
     std::vector<uint8_t> sel_r, sel_c;
     const bool joint = !mode_col && !mode_row && !mode_block;
     if (joint) block_cover(nr, nc, ap, adj, colmax, sel_r, sel_c);
+    // SHIRO_F_COVER_BALANCE (R18): near-minimum all-rows cover -> all rows
+    bool all_rows = false;
+    if (joint && (in.flags & SHIRO_F_COVER_BALANCE)) {
+      int64_t mu = 0;
+      for (uint8_t x : sel_r) mu += x;
+      for (uint8_t x : sel_c) mu += x;
+      all_rows = nr <= mu + std::max<int64_t>(1, mu / 1000);
+    }
     // assignment (P3)
     std::vector<uint8_t> row_used(nr, 0), col_used(nc, 0);
     int64_t nrow_nz = 0;
@@ -186,7 +194,7 @@ Phase1 plan_phase1(const PlanInput &in) {
         const int32_t v = adj[e];
         bool is_row;
         if (mode_col || mode_block) is_row = false;
-        else if (mode_row) is_row = true;
+        else if (mode_row || all_rows) is_row = true;
         else if (!colmax) is_row = sel_r[u];
         else is_row = !sel_c[v];
         const int64_t k = idx[b0 + e];
@@ -201,7 +209,13 @@ Phase1 plan_phase1(const PlanInput &in) {
       for (int64_t x = 0; x < Kq; ++x) b_ids.push_back(qlo + x);
     for (int32_t u = 0; u < nr; ++u)
       if (row_used[u]) c_ids.push_back(lo + urow[u]);
-    if (joint) {
+    if (joint && all_rows) {
+      // balanced all-rows cover: every row carries its nonzeros, no column is sent
+      for (int32_t u = 0; u < nr; ++u)
+        if (!row_used[u]) throw Error(SHIRO_E_INTERNAL, "balanced cover: row unused");
+      for (int32_t v = 0; v < nc; ++v)
+        if (col_used[v]) throw Error(SHIRO_E_INTERNAL, "balanced cover: column used");
+    } else if (joint) {
       // every selected vertex carries a private edge (minimality)
       for (int32_t u = 0; u < nr; ++u)
         if (sel_r[u] != row_used[u]) throw Error(SHIRO_E_INTERNAL, "selected row unused");

@@ -48,7 +48,8 @@ def main():
     flags = 0
     for f in filter(None, args.flags.split(",")):
         flags |= {"split": sh.F_SPLIT_RECV, "colmax": sh.F_COVER_COLMAX, "col": sh.F_MODE_COL,
-                  "row": sh.F_MODE_ROW, "nooverlap": sh.F_NO_OVERLAP, "nccl": sh.F_XCHG_NCCL}[f]
+                  "row": sh.F_MODE_ROW, "nooverlap": sh.F_NO_OVERLAP, "nccl": sh.F_XCHG_NCCL,
+                  "balance": sh.F_COVER_BALANCE}[f]
     obj = [sh.get_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     pl = sh.Plan.distributed(rank, world, cfg.n, part, rp_l, col_l, val_l, cfg.N,
@@ -62,7 +63,8 @@ def main():
     # lists vs oracle (every rank checks its own)
     op = None if args.no_lists else oracle.plan_flat(cfg.n, part, row_ptr, col,
                           mode="col" if flags & sh.F_MODE_COL else "row" if flags & sh.F_MODE_ROW else "joint",
-                          rule="colmax" if flags & sh.F_COVER_COLMAX else "rowmax")
+                          rule="colmax" if flags & sh.F_COVER_COLMAX else "rowmax",
+                          balance=bool(flags & sh.F_COVER_BALANCE))
     empty = np.empty(0, np.int64)
     lists_ok = True
     for p in range(world if op is not None else 0):

@@ -114,7 +114,7 @@ def test_empty_and_degenerate():
 @pytest.mark.parametrize("P", [2, 3, 4, 8])
 @pytest.mark.parametrize("flags", [0, sh.F_SPLIT_RECV, sh.F_COVER_COLMAX, sh.F_MODE_COL,
                                    sh.F_MODE_ROW, sh.F_MODE_BLOCK, sh.F_XCHG_NCCL,
-                                   sh.F_XCHG_NCCL | sh.F_SPLIT_RECV])
+                                   sh.F_XCHG_NCCL | sh.F_SPLIT_RECV, sh.F_COVER_BALANCE])
 def test_loopback_random_integer_exact(P, flags):
     rng = np.random.default_rng(P * 100 + flags)
     n, N = 2000, 64
