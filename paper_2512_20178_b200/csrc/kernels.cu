@@ -544,8 +544,8 @@ void spmm_shape(const SpmmArgs &a, bool acc, cudaStream_t s) {
     default: break;
   }
 #endif
-  switch (spmm_variant()) {   // CTA-size variants
-    case 4: spmm_launch<LPR, VPL, 5, 4>(a, acc, s); return;          // 8-warp CTAs, 48 regs
+#ifdef SHIRO_KERNEL_SWEEP
+  switch (spmm_variant()) {   // CTA-size variants (profiles/r1_kernel_sweep.txt)
     case 11: spmm_launch<LPR, VPL, 20, 4, 64>(a, acc, s); return;
     case 12: spmm_launch<LPR, VPL, 10, 4, 128>(a, acc, s); return;
     case 13: spmm_launch<LPR, VPL, 16, 8, 64>(a, acc, s); return;
@@ -554,6 +554,11 @@ void spmm_shape(const SpmmArgs &a, bool acc, cudaStream_t s) {
     case 17: spmm_launch<LPR, VPL, 24, 8, 32>(a, acc, s); return;
     case 18: spmm_launch<LPR, VPL, 24, 4, 32>(a, acc, s); return;
     default: break;
+  }
+#endif
+  if (spmm_variant() == 4) {   // round-1 baseline: 8-warp CTAs, 48 regs (SHIRO_KERNEL=4)
+    spmm_launch<LPR, VPL, 5, 4>(a, acc, s);
+    return;
   }
   // measured best (profiles/r1_kernel_sweep.txt): one-warp CTAs, 32 per SM
   // (the per-SM CTA limit), 64 registers without spills.  A CTA retires as
@@ -568,8 +573,10 @@ void spmm_shape(const SpmmArgs &a, bool acc, cudaStream_t s) {
   static const int env_hint = getenv("SHIRO_L2HINT") ? atoi(getenv("SHIRO_L2HINT")) : -1;
   const int hint = env_hint >= 0 ? env_hint
                                  : ((a.X1 == nullptr && a.n0 * (int64_t)a.N * 4 <= (96ll << 20)) ? 2 : 0);
-  if (LPR == 32 && VPL == 1 && hint == 1) { spmm_launch<LPR, VPL, 32, 4, 32, 1>(a, acc, s); return; }
-  if (LPR == 32 && VPL == 1 && hint == 2) { spmm_launch<LPR, VPL, 32, 4, 32, 2>(a, acc, s); return; }
+  if constexpr (LPR == 32 && VPL == 1) {
+    if (hint == 1) { spmm_launch<LPR, VPL, 32, 4, 32, 1>(a, acc, s); return; }
+    if (hint == 2) { spmm_launch<LPR, VPL, 32, 4, 32, 2>(a, acc, s); return; }
+  }
   spmm_launch<LPR, VPL, 32, 4, 32>(a, acc, s);
 }
 

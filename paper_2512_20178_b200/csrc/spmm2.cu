@@ -291,16 +291,19 @@ int launch_spmm2(const SpmmArgs &a, bool accumulate, cudaStream_t s) {
   const int var = kernel_choice();
   switch (a.N) {
     case 128:
-      switch (var) {   // (U, MINB) variants for tuning sweeps; default measured best
+#ifdef SHIRO_KERNEL_SWEEP
+      switch (var) {   // (U, MINB, CTA size) variants of the sweeps
         case 3: launch2<32, 4, 3>(a, accumulate, s); return 1;
-        case 4: launch2<32, 2, 5>(a, accumulate, s); return 1;
         case 5: launch2<32, 2, 6>(a, accumulate, s); return 1;
         case 6: launch2<32, 2, 20, 64>(a, accumulate, s); return 1;
         case 7: launch2<32, 4, 16, 64>(a, accumulate, s); return 1;
         case 8: launch2<32, 4, 24, 32>(a, accumulate, s); return 1;
         case 9: launch2<32, 2, 32, 32>(a, accumulate, s); return 1;
-        default: launch2<32, 4, 4>(a, accumulate, s); return 1;
+        default: break;
       }
+#endif
+      launch2<32, 4, 4>(a, accumulate, s);
+      return 1;
     case 64: launch2<16, 4, 4>(a, accumulate, s); return 1;
     case 32: launch2<8, 4, 4>(a, accumulate, s); return 1;
     default: return 0;

@@ -52,7 +52,8 @@ def main():
     only = set(filter(None, os.environ.get("ABLATION_ONLY", "").split(",")))
     strategies = [("block", sh.F_MODE_BLOCK, 1), ("col", sh.F_MODE_COL, 1),
                   ("row", sh.F_MODE_ROW, 1), ("joint", 0, 1),
-                  ("joint-colmax", sh.F_COVER_COLMAX, 1)]
+                  ("joint-colmax", sh.F_COVER_COLMAX, 1),
+                  ("joint-balanced", sh.F_COVER_BALANCE, 1)]
     if args.group_size > 1 and world % args.group_size == 0 and world > args.group_size:
         strategies.append((f"joint+hier(g={args.group_size})", 0, args.group_size))
     records = []
