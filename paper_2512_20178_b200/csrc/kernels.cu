@@ -119,6 +119,31 @@ __device__ __noinline__ void sig_unit_done(int32_t *ctr, int32_t target, const i
 #define SHIRO_SIG_DONE(a, li, mask) \
   sig_unit_done((a).sig_ctr, (a).sig_target, (a).sig_epoch, (a).sig_ptrs, (a).sig_n, li, mask)
 
+// In-kernel READY wait of the consumer (SpmmArgs::wait_*), whole warp.
+__device__ __noinline__ bool wait_flags_ready(const int32_t *flags, int32_t n,
+                                              const int32_t *epoch, int32_t *err,
+                                              int64_t timeout_ns, int lane) {
+  const int32_t value = *epoch;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+  for (;;) {
+    bool ok = true;
+    for (int i = lane; i < n; i += 32) {
+      int32_t v;
+      asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(flags + i) : "memory");
+      ok = ok && v >= value;
+    }
+    if (__all_sync(0xffffffffu, ok)) return true;
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    if ((int64_t)(t - t0) > timeout_ns) {
+      if (lane == 0) atomicExch(err, 1);
+      return false;
+    }
+    __nanosleep(256);
+  }
+}
+
 // Output row address of a pointer-routed row: a peer (or own) buffer address,
 // or -- top bit set -- a row index into Y (the caller's C: local rows of the
 // fused producer launch, whose address is only known at call time).
@@ -313,6 +338,9 @@ __global__ void __launch_bounds__(BS, MINB) k_spmm(const SpmmArgs a) {
   const int li = lane % LPR;
   const unsigned mask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (sub * LPR));
   const int64_t warp = ((int64_t)blockIdx.x * BS + threadIdx.x) >> 5;
+  if (ACCUM && a.wait_flags &&
+      !wait_flags_ready(a.wait_flags, a.wait_n, a.wait_epoch, a.wait_err, a.wait_timeout_ns, lane))
+    return;
   spmm_unit<LPR, VPL, ACCUM, TWO, (U < LPR ? U : LPR), OUTP, HINT>(a, warp * R + sub, li, mask);
 }
 

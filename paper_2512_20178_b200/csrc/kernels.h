@@ -53,6 +53,14 @@ struct SpmmArgs {
   int32_t *sig_ctr = nullptr;           // zero-initialised, re-armed by the signaller
   int32_t *const *sig_ptrs = nullptr;
   const int32_t *sig_epoch = nullptr;
+  // In-kernel wait (fused exchange consumer): before its unit, every warp
+  // spins until wait_flags[0..wait_n) >= *wait_epoch (ld.acquire.sys), with a
+  // %globaltimer timeout that sets *wait_err instead of hanging.  nullptr: off.
+  const int32_t *wait_flags = nullptr;
+  int32_t wait_n = 0;
+  const int32_t *wait_epoch = nullptr;
+  int32_t *wait_err = nullptr;
+  int64_t wait_timeout_ns = 0;
 };
 
 // accumulate: false -> Y = A*X (overwrite, empty rows get zeros); true -> Y += A*X

@@ -615,6 +615,17 @@ bool fused_step_enabled() {
   return v == 1;
 }
 
+// SHIRO_INKERNEL_WAIT=1: the remote SpMM waits for READY itself (one launch
+// fewer per step; opt-in until measured)
+bool inkernel_wait_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("SHIRO_INKERNEL_WAIT");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 // SHIRO_EARLY_READY=1: the producer raises READY from inside its launch once
 // the peer-destined units are stored.  Opt-in: measured slower at P=2 (c4
 // 1.66 vs 1.55 ms, c3 2.81 vs 2.67 ms, profiles/r1_early_ready_P2.txt): the
@@ -652,6 +663,28 @@ void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
     prod.a.out_ptr = pl.prod_out_ptr[par];
     launches += run_spmm(prod, B, pl.M, nullptr, C, false, s);
     rec(6);
+    int lpr_, vpl_;
+    if (inkernel_wait_enabled() && !(pl.flags & SHIRO_F_SPLIT_RECV) && pl.d_rem.a.nrows > 0 &&
+        !pl.prof_on && vec_shape(pl.N, &lpr_, &vpl_)) {
+      // READY = e with the epoch advanced by the signal kernel; the remote
+      // SpMM's warps wait for READY >= e themselves (3 launches per step)
+      launches += launch_signal(pl.ready_ptrs, P - 1, ep, 1, true, s);
+      rec(3);
+      rec(4);
+      DevSpmm rem = pl.d_rem;
+      rem.a.wait_flags = pl.xflags;
+      rem.a.wait_n = P;
+      rem.a.wait_epoch = ep;
+      rem.a.wait_err = err;
+      rem.a.wait_timeout_ns = pl.wait_timeout_ns;
+      launches += run_spmm(rem, rb, pl.recv_rows, nullptr, C, true, s);
+      rec(7);
+      rec(8);
+      SHIRO_CK(cudaMemcpyAsync(pl.err_host, err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      pl.last_launches = launches;
+      pl.prof_used = 3;
+      return;
+    }
     launches += launch_signal(pl.ready_ptrs, P - 1, ep, 1, false, s);
     rec(3);
     launches += launch_wait(pl.xflags, P, ep, 1, err, pl.wait_timeout_ns, s, true);

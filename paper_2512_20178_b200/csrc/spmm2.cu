@@ -287,7 +287,7 @@ int launch_spmm2(const SpmmArgs &a, bool accumulate, cudaStream_t s) {
   // opt-in (SHIRO_KERNEL=2,3,5..9): measured slower than k_spmm with one-warp
   // CTAs (profiles/r1_kernel_sweep.txt)
   const int kc = kernel_choice();
-  if (kc < 2 || kc == 4 || kc >= 10 || a.sig_ptrs) return 0;   // no early-READY support
+  if (kc < 2 || kc == 4 || kc >= 10 || a.sig_ptrs || a.wait_flags) return 0;   // no in-kernel flags
   const int var = kernel_choice();
   switch (a.N) {
     case 128:
