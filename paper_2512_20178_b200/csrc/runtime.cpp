@@ -615,13 +615,14 @@ bool fused_step_enabled() {
   return v == 1;
 }
 
-// SHIRO_INKERNEL_WAIT=1: the remote SpMM waits for READY itself (one launch
-// fewer per step; opt-in until measured)
+// The remote SpMM's warps wait for READY themselves (one launch fewer per
+// step: c2/P=4 0.074 -> 0.068 ms, c4 -0.5 %, profiles/r1_inkernel_wait_P4.txt);
+// SHIRO_INKERNEL_WAIT=0 keeps the separate k_wait launch
 bool inkernel_wait_enabled() {
   static int v = -1;
   if (v < 0) {
     const char *e = getenv("SHIRO_INKERNEL_WAIT");
-    v = (e && e[0] == '1') ? 1 : 0;
+    v = (e && e[0] == '0') ? 0 : 1;
   }
   return v == 1;
 }

@@ -91,8 +91,8 @@ def _run(world, flags=0, env=None):
     return sorted(q.get() for _ in range(world))
 
 
-@pytest.mark.parametrize("env", [{}, {"SHIRO_DBUF": "0"}, {"SHIRO_INKERNEL_WAIT": "1"}],
-                         ids=["double-buffered", "single-buffer", "in-kernel-wait"])
+@pytest.mark.parametrize("env", [{}, {"SHIRO_DBUF": "0"}, {"SHIRO_INKERNEL_WAIT": "0"}],
+                         ids=["default", "single-buffer", "separate-wait-launch"])
 def test_two_process_fused_exchange_exact(env):
     import paper_2512_20178_b200 as sh
     for flags in (0, sh.F_SPLIT_RECV):
