@@ -148,6 +148,7 @@ typedef struct {
    * rows), output rows and distinct source rows read -- the algorithmic
    * traffic of each kernel launch */
   int64_t op_nnz[5], op_rows[5], op_src_rows[5];
+  double refresh_seconds;   /* wall time of the last value refresh (0 if none)   */
 } shiro_info_t;
 #define SHIRO_OP_LOCAL 0   /* K1: A_diag * B_local             */
 #define SHIRO_OP_PARTIAL 1 /* K3: A_out * B_local -> send_buf   */
@@ -176,10 +177,53 @@ int shiro_plan(const shiro_dist_t *d, int64_t n, const int64_t *part, const int6
                shiro_plan_t *out);
 
 /*
+ * Weighted covers (Eqs. 4-8, and the weighted network of
+ * L372-375): as shiro_plan, but block covers minimise
+ *     sum_{selected C rows i} w_row[i] + sum_{selected B rows j} w_col[j]
+ * instead of the row count (exact minimum s-t cut by Dinic's algorithm; the
+ * canonical s-reachable read-off of DESIGN.md R1 applies unchanged).
+ *   w_row  host int64[M_p]: cost of communicating a partial C row of each of
+ *          this rank's rows (local row index), every used entry > 0
+ *   w_col  host int64[n]:   cost of communicating B row j (global id), > 0;
+ *          entries of columns this rank's rows do not reference are unused
+ * With SHIRO_F_TRANSPOSE the weights refer to the planned matrix A^T.
+ * Weights only affect joint-mode covers (ignored by SHIRO_F_MODE_*).
+ * Errors: as shiro_plan; SHIRO_E_ARG if a weight pointer is NULL or a used
+ * weight is <= 0 (detected while planning the block on that rank).
+ */
+int shiro_plan_weighted(const shiro_dist_t *d, int64_t n, const int64_t *part,
+                        const int64_t *row_ptr, const int32_t *col_idx, const float *val, int32_t N,
+                        const int64_t *w_row, const int64_t *w_col, void *stream,
+                        shiro_plan_t *out);
+
+/*
+ * Value refresh for a fixed sparsity pattern (the plan "can be
+ * reused across multiple SpMM operations with the same sparsity pattern";
+ * SURVEY 8(f) N3).  Collective.  `val` holds the new values of this rank's
+ * nonzeros, in the order of the col_idx array given to shiro_plan (same
+ * row_ptr / col_idx pattern).  The cover, lists and device layouts are kept;
+ * each rank re-ships only the values of its row-based nonzeros (4 B each, one
+ * all-to-allv over the plan's transport) and rewrites the values of its
+ * device operations in place.  Returns after the device copy is updated
+ * (synchronous on `stream`); the next shiro_spmm uses the new values.
+ * row_ptr / col_idx: only read for SHIRO_F_TRANSPOSE plans (the values are
+ * redistributed like the plan-time transpose), may be NULL otherwise.
+ * A plan built with a host transport (host_xchg) keeps using it here: the
+ * callback and its context must stay valid for the plan's lifetime.
+ * Errors: SHIRO_E_ARG (loopback or HOST_ONLY plan, NULL val), SHIRO_E_NCCL /
+ * SHIRO_E_TRANSPORT (exchange), SHIRO_E_CUDA.
+ */
+int shiro_plan_update_values(shiro_plan_t plan, const int64_t *row_ptr, const int32_t *col_idx,
+                             const float *val, void *stream);
+
+/*
  * One distributed SpMM: C_p = A^(p,:) * B.  Collective, stream-ordered,
  * asynchronous.  B_p: device fp32 [M_p x N] row-major, read-only until the
  * stream passes this call.  C_p: device fp32 [M_p x N], fully overwritten.
- * Both 16-byte aligned.
+ * Both 16-byte aligned.  A peer that fails to signal within the timeout
+ * (SHIRO_P2P_TIMEOUT_MS, default 20 s) is reported by the NEXT call on this
+ * plan (SHIRO_E_PEER), since this call returns before the device runs; the
+ * host-buffer calls below synchronise and report it themselves.
  */
 int shiro_spmm(shiro_plan_t plan, const float *B_p, float *C_p, void *stream);
 
@@ -226,6 +270,15 @@ int shiro_plan_loopback(int32_t nranks, int32_t group_size, uint32_t flags, int6
                         const int64_t *part, const int64_t *row_ptr, const int32_t *col_idx,
                         const float *val, int32_t N, void *stream, shiro_plan_t *out);
 int shiro_spmm_loopback(shiro_plan_t plan, const float *B, float *C, void *stream);
+/* Loopback variants of shiro_plan_weighted (w_row: int64[n], all rows) and
+ * shiro_plan_update_values (val: the full matrix's new values, same order as
+ * the col_idx given to shiro_plan_loopback). */
+int shiro_plan_loopback_weighted(int32_t nranks, int32_t group_size, uint32_t flags, int64_t n,
+                                 const int64_t *part, const int64_t *row_ptr,
+                                 const int32_t *col_idx, const float *val, int32_t N,
+                                 const int64_t *w_row, const int64_t *w_col, void *stream,
+                                 shiro_plan_t *out);
+int shiro_plan_update_values_loopback(shiro_plan_t plan, const float *val, void *stream);
 /* Borrowed view of virtual rank r of a loopback plan (do not free). */
 int shiro_plan_rank(shiro_plan_t plan, int32_t r, shiro_plan_t *out);
 
@@ -234,11 +287,16 @@ int shiro_plan_rank(shiro_plan_t plan, int32_t r, shiro_plan_t *out);
  * stage; shiro_stage_times waits for the last call and writes the durations
  * in milliseconds, indexed by SHIRO_STAGE_* (0 for stages that did not run).
  * Distributed plans only. */
-#define SHIRO_STAGE_PACK 0     /* E1: K4 pack of B rows                        */
-#define SHIRO_STAGE_PARTIAL 1  /* E2: K3 row-based partial SpMM                */
-#define SHIRO_STAGE_EXCHANGE 2 /* E3: NCCL all-to-allv (communication stream)  */
-#define SHIRO_STAGE_LOCAL 3    /* E4: K1 local SpMM                            */
-#define SHIRO_STAGE_REMOTE 4   /* E5: K2 (or fused K2+K5) remote SpMM          */
+#define SHIRO_STAGE_PACK 0     /* E1: K4 pack of B rows (NCCL exchange)        */
+#define SHIRO_STAGE_PARTIAL 1  /* E2: K3 row-based partial SpMM; fused exchange:
+                                  the producer launch (K4 + K3 -> peers)       */
+#define SHIRO_STAGE_EXCHANGE 2 /* E3: NCCL all-to-allv (communication stream);
+                                  fused exchange: the READY signal             */
+#define SHIRO_STAGE_LOCAL 3    /* E4: K1 local SpMM (fused exchange: measured
+                                  from the step's start, concurrent with the
+                                  producer)                                    */
+#define SHIRO_STAGE_REMOTE 4   /* E5: K2 (or fused K2+K5) remote SpMM, incl. its
+                                  per-source waits                             */
 #define SHIRO_STAGE_SCATTER 5  /* E6: K5 scatter-add                           */
 #define SHIRO_STAGE_TOTAL 6    /* first event to last event                    */
 #define SHIRO_NUM_STAGES 7

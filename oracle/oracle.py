@@ -132,15 +132,19 @@ def min_cover_local(nr: int, nc: int, er, ec, w_row=None, w_col=None, rule="rowm
     return sr[:nr].astype(bool), sc[:nc].astype(bool), int(flow.value)
 
 
-def min_cover(gi, gj, rule="rowmax"):
-    """Uniform-weight cover of a block given by its edges in global ids.
+def min_cover(gi, gj, rule="rowmax", w_row=None, w_col=None):
+    """Cover of a block given by its edges in global ids.
     Rows = Rows(A^(p,q)), Cols = Cols(A^(p,q)) (Table I).
-    Returns (selected rows ascending, selected cols ascending, mu)."""
+    Uniform weights unless w_row / w_col (indexed by GLOBAL row / column
+    id) give the per-vertex costs w^row_i, w^col_j of Eqs. 4-6.
+    Returns (selected rows ascending, selected cols ascending, flow)."""
     rows = np.unique(gi)
     cols = np.unique(gj)
     li = np.searchsorted(rows, gi)
     lj = np.searchsorted(cols, gj)
-    sr, sc, f = min_cover_local(rows.size, cols.size, li, lj, rule=rule)
+    wr = None if w_row is None else np.asarray(w_row, np.int64)[rows]
+    wc = None if w_col is None else np.asarray(w_col, np.int64)[cols]
+    sr, sc, f = min_cover_local(rows.size, cols.size, li, lj, w_row=wr, w_col=wc, rule=rule)
     return rows[sr], cols[sc], f
 
 
@@ -222,7 +226,8 @@ def balance_slack(mu):
     return max(1, int(mu) // 1000)
 
 
-def plan_flat(n, part, row_ptr, col, mode="joint", rule="rowmax", balance=False) -> FlatPlan:
+def plan_flat(n, part, row_ptr, col, mode="joint", rule="rowmax", balance=False, w_row=None,
+              w_col=None) -> FlatPlan:
     """Per ordered pair (p, q), p != q, decide per nonzero ROW vs COL.
 
     joint: canonical min cover of A^(p,q) (R1); nonzero (i,j) is
@@ -237,6 +242,9 @@ def plan_flat(n, part, row_ptr, col, mode="joint", rule="rowmax", balance=False)
       nonzero of the block is ROW (the column owner q computes the block), so
       dense-ish symmetric blocks are computed by alternating sides instead of
       all on one rank; bytes rise by at most the slack per block.
+    w_row, w_col (joint only): per-vertex costs indexed by global row / column
+      id (Eqs. 4-6); the block cover is then the minimum-weight
+      cover of the weighted network of P:372-375, read off the same way (R1).
     Lists: send_b[(q,p)] = selected cols, send_c[(q,p)] = selected rows,
     global ids ascending."""
     part = np.asarray(part, np.int64)
@@ -265,12 +273,15 @@ def plan_flat(n, part, row_ptr, col, mode="joint", rule="rowmax", balance=False)
             plan.n_rows[(q, p)] = rows_u.size
             plan.n_cols[(q, p)] = cols_u.size
             if mode == "joint":
-                sel_r, sel_c, mu = min_cover(bi, bj, rule=rule)
+                sel_r, sel_c, mu = min_cover(bi, bj, rule=rule, w_row=w_row, w_col=w_col)
                 if rule == "rowmax":
                     is_row = np.isin(bi, sel_r)
                 else:
                     is_row = ~np.isin(bj, sel_c)
-                assert sel_r.size + sel_c.size == mu
+                if w_row is None:
+                    assert sel_r.size + sel_c.size == mu
+                else:
+                    mu = sel_r.size + sel_c.size        # rows moved, not the cut weight
                 if balance and rows_u.size <= mu + balance_slack(mu):
                     is_row = np.ones(idx.size, bool)
             elif mode == "col":

@@ -69,7 +69,8 @@ class InfoT(ctypes.Structure):
     _fields_ = ([(f, ctypes.c_int32) for f in _INFO_FIELDS] +
                 [(f, ctypes.c_int64) for f in _INFO_FIELDS64] +
                 [("plan_seconds", ctypes.c_double)] +
-                [(f, ctypes.c_int64 * 5) for f in ("op_nnz", "op_rows", "op_src_rows")])
+                [(f, ctypes.c_int64 * 5) for f in ("op_nnz", "op_rows", "op_src_rows")] +
+                [("refresh_seconds", ctypes.c_double)])
 
 OPS = ("local", "partial", "remote", "scatter", "pack")
 
@@ -90,6 +91,12 @@ def load():
     sig = {
         "shiro_get_unique_id": [P],
         "shiro_plan": [ctypes.POINTER(DistT), I64, P, P, P, P, I32, P, ctypes.POINTER(P)],
+        "shiro_plan_weighted": [ctypes.POINTER(DistT), I64, P, P, P, P, I32, P, P, P,
+                                ctypes.POINTER(P)],
+        "shiro_plan_update_values": [P, P, P, P, P],
+        "shiro_plan_loopback_weighted": [I32, I32, U32, I64, P, P, P, P, I32, P, P, P,
+                                         ctypes.POINTER(P)],
+        "shiro_plan_update_values_loopback": [P, P, P],
         "shiro_spmm": [P, P, P, P],
         "shiro_spmm_host": [P, P, P, P],
         "shiro_spmm_host_batch": [P, I64, P, P, P],
@@ -173,10 +180,12 @@ class Plan:
     # ---------------------------------------------------------------- build
     @classmethod
     def distributed(cls, rank, nranks, n, part, row_ptr, col, val, N, group_size=1, flags=0,
-                    nccl_id=None, host_xchg=None, stream=None):
-        """shiro_plan: this rank's CSR rows (global column ids).  ``host_xchg``:
+                    nccl_id=None, host_xchg=None, stream=None, w_row=None, w_col=None):
+        """shiro_plan (or shiro_plan_weighted with w_row [M_p] / w_col [n]
+        int64 costs): this rank's CSR rows (global column ids).  ``host_xchg``:
         optional Python all-to-allv (list of bytes per peer -> list of bytes)
-        used for the plan-time exchange (e.g. over gloo)."""
+        used for the plan-time exchange (e.g. over gloo) and later value
+        refreshes."""
         lib = load()
         part = np.ascontiguousarray(part, dtype=np.int64)
         row_ptr, col, val = _host_arrays(row_ptr, col, val)
@@ -192,23 +201,58 @@ class Plan:
             d.host_xchg = cb
         out = ctypes.c_void_p()
         s = ctypes.c_void_p(0) if flags & F_HOST_ONLY else _stream_ptr(stream)
-        _check(lib.shiro_plan(ctypes.byref(d), n, _np_ptr(part), _np_ptr(row_ptr), _np_ptr(col),
-                              _np_ptr(val), N, s, ctypes.byref(out)))
+        if w_row is None and w_col is None:
+            _check(lib.shiro_plan(ctypes.byref(d), n, _np_ptr(part), _np_ptr(row_ptr),
+                                  _np_ptr(col), _np_ptr(val), N, s, ctypes.byref(out)))
+        else:
+            wr = np.ascontiguousarray(w_row, dtype=np.int64)
+            wc = np.ascontiguousarray(w_col, dtype=np.int64)
+            _check(lib.shiro_plan_weighted(ctypes.byref(d), n, _np_ptr(part), _np_ptr(row_ptr),
+                                           _np_ptr(col), _np_ptr(val), N, _np_ptr(wr),
+                                           _np_ptr(wc), s, ctypes.byref(out)))
         return cls(out.value, True, keep)
 
     @classmethod
     def loopback(cls, nranks, n, part, row_ptr, col, val, N, group_size=1, flags=0,
-                 stream=None):
-        """shiro_plan_loopback: all virtual ranks on one device (full CSR)."""
+                 stream=None, w_row=None, w_col=None):
+        """shiro_plan_loopback (shiro_plan_loopback_weighted with w_row [n] /
+        w_col [n] int64 costs): all virtual ranks on one device (full CSR)."""
         lib = load()
         part = np.ascontiguousarray(part, dtype=np.int64)
         row_ptr, col, val = _host_arrays(row_ptr, col, val)
         out = ctypes.c_void_p()
         s = ctypes.c_void_p(0) if flags & F_HOST_ONLY else _stream_ptr(stream)
-        _check(lib.shiro_plan_loopback(nranks, group_size, flags, n, _np_ptr(part),
-                                       _np_ptr(row_ptr), _np_ptr(col), _np_ptr(val), N, s,
-                                       ctypes.byref(out)))
-        return cls(out.value, True)
+        if w_row is None and w_col is None:
+            _check(lib.shiro_plan_loopback(nranks, group_size, flags, n, _np_ptr(part),
+                                           _np_ptr(row_ptr), _np_ptr(col), _np_ptr(val), N, s,
+                                           ctypes.byref(out)))
+        else:
+            wr = np.ascontiguousarray(w_row, dtype=np.int64)
+            wc = np.ascontiguousarray(w_col, dtype=np.int64)
+            _check(lib.shiro_plan_loopback_weighted(nranks, group_size, flags, n, _np_ptr(part),
+                                                    _np_ptr(row_ptr), _np_ptr(col),
+                                                    _np_ptr(val), N, _np_ptr(wr), _np_ptr(wc), s,
+                                                    ctypes.byref(out)))
+        pl = cls(out.value, True)
+        pl._loopback = True
+        return pl
+
+    def update_values(self, val, row_ptr=None, col=None, stream=None):
+        """shiro_plan_update_values (distributed; row_ptr/col needed only for
+        SHIRO_F_TRANSPOSE plans) or shiro_plan_update_values_loopback."""
+        val = np.ascontiguousarray(val, dtype=np.float32)
+        lib = load()
+        if self._is_loopback():
+            _check(lib.shiro_plan_update_values_loopback(self._h, _np_ptr(val),
+                                                         _stream_ptr(stream)))
+            return
+        rp = None if row_ptr is None else np.ascontiguousarray(row_ptr, dtype=np.int64)
+        cl = None if col is None else np.ascontiguousarray(col, dtype=np.int32)
+        _check(lib.shiro_plan_update_values(self._h, _np_ptr(rp), _np_ptr(cl), _np_ptr(val),
+                                            _stream_ptr(stream)))
+
+    def _is_loopback(self):
+        return getattr(self, "_loopback", False)
 
     # ---------------------------------------------------------------- run
     def spmm(self, B, C, stream=None):

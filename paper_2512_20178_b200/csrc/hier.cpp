@@ -308,7 +308,8 @@ void hier_build(const PlanInput &in, const Phase1 &p1, Plan &pl,
   for (int64_t t = 0; t < R.s2_agg.nrows; ++t) R.s2_agg.out_row.push_back((int32_t)t);
   // ---- final remote SpMM over [R1 || R2] ------------------------------------------
   // COL entries by B-row location, then unit-weight partials
-  std::vector<std::vector<std::pair<int32_t, float>>> rows(M);
+  struct FinEnt { int32_t pos; float v; int32_t k; };   // k: value-space index (-1 = unit)
+  std::vector<std::vector<FinEnt>> rows(M);
   for (int64_t t = 0; t < M; ++t) {
     for (int64_t k = in.row_ptr[t]; k < in.row_ptr[t + 1]; ++k) {
       if (p1.tag[k] != 2) continue;
@@ -322,7 +323,7 @@ void hier_build(const PlanInput &in, const Phase1 &p1, Plan &pl,
         const int s = G0 * g + q % g;
         pos = R.r1_rows + r2_fwd_base.at({s, q}) + index_of(pl.recv_b[q], j);
       }
-      rows[t].push_back({(int32_t)pos, in.val[k]});
+      rows[t].push_back({(int32_t)pos, in.val[k], (int32_t)k});
     }
   }
   for (int s = 0; s < P; ++s) {
@@ -330,16 +331,20 @@ void hier_build(const PlanInput &in, const Phase1 &p1, Plan &pl,
     if (in_g0(s)) {
       const int64_t base = r1_c_base.at({s, me});
       for (size_t k = 0; k < pl.recv_c[s].size(); ++k)
-        rows[pl.recv_c[s][k] - lo].push_back({(int32_t)(base + k), 1.0f});
+        rows[pl.recv_c[s][k] - lo].push_back({(int32_t)(base + k), 1.0f, -1});
     } else if (s % g == me % g) {
       const auto &V = Vin[s];
       for (size_t k = 0; k < V.size(); ++k)
-        rows[V[k] - lo].push_back({(int32_t)(R.r1_rows + r2_agg_base.at(s) + k), 1.0f});
+        rows[V[k] - lo].push_back({(int32_t)(R.r1_rows + r2_agg_base.at(s) + k), 1.0f, -1});
     }
   }
   for (int64_t t = 0; t < M; ++t) {
     if (rows[t].empty()) continue;
-    for (auto &e : rows[t]) { R.fin.col.push_back(e.first); R.fin.val.push_back(e.second); }
+    for (auto &e : rows[t]) {
+      R.fin.col.push_back(e.pos);
+      R.fin.val.push_back(e.v);
+      R.fin.vsrc.push_back(e.k);
+    }
     R.fin.rp.push_back((int64_t)R.fin.col.size());
     R.fin.out_row.push_back((int32_t)t);
   }

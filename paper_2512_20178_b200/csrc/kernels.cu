@@ -9,7 +9,7 @@
 //     with one 128-bit load per lane (fully coalesced LDG.128);
 //   * the nonzeros of a work unit are loaded cooperatively as interleaved
 //     (col, val) pairs, one 8-byte streaming load per lane, and broadcast with
-//     shuffles; U = 8 independent row gathers are issued before any FMA;
+//     shuffles; U = 4 independent row gathers are issued before any FMA;
 //   * short rows are packed at plan time into row groups (<= L nonzeros,
 //     <= 64 rows); a per-nonzero byte gives the row offset inside the group,
 //     so row boundaries cost no memory access and the gathers of many short
@@ -18,7 +18,14 @@
 //     nonzeros scheduled first; their partials are reduced in chunk order by
 //     the last-arriving chunk (threadfence + arrival counter): deterministic,
 //     single launch;
-//   * fp32 accumulation in registers, one store per output row.
+//   * fp32 accumulation in registers, one store per output row;
+//   * one-warp CTAs, 32 resident per SM (measured best).
+// L2 policy per launch (HINT): 0 default; 2 = source rows fit in L2 -> the
+// streams (A's (col, val) pairs, C rows) evict_first, gathered rows
+// evict_last; 3 = source rows far larger than L2 -> the plan-time "hot" rows
+// (bit 31 of the column id) evict_last, every other gather and the streams
+// evict_first.  WAIT: per-unit, per-source READY wait of the fused exchange
+// consumer with L2-coherent source loads (SpmmArgs::ready).
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -31,18 +38,8 @@ namespace shiro {
 
 namespace {
 
-constexpr int kBlock = 256;   // 8 warps per CTA
+constexpr int kBlock = 256;   // CTA size of the pack / scatter / generic kernels
 
-__device__ __forceinline__ int2 ld_stream_cv(const int2 *p) {
-  int2 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.s32 {%0, %1}, [%2];"
-               : "=r"(v.x), "=r"(v.y)
-               : "l"(p));
-  return v;
-}
-// L2 eviction-policy variants (HINT, SHIRO_L2HINT): 0 = default policies;
-// 1 = the streams read or written once (A's (col, val) pairs, C rows) are
-// L2 evict_first; 2 = 1 + the gathered B rows evict_last.
 __device__ __forceinline__ uint64_t pol_first() {
   uint64_t p;
   asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -55,20 +52,36 @@ __device__ __forceinline__ uint64_t pol_last() {
 }
 template <int HINT>
 __device__ __forceinline__ int2 ldcv_h(const int2 *p) {
-  if (HINT == 0) return ld_stream_cv(p);
   int2 v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;"
-               : "=r"(v.x), "=r"(v.y)
-               : "l"(p), "l"(pol_first()));
+  if (HINT == 0) {
+    asm volatile("ld.global.nc.L1::no_allocate.v2.s32 {%0, %1}, [%2];"
+                 : "=r"(v.x), "=r"(v.y)
+                 : "l"(p));
+  } else {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;"
+                 : "=r"(v.x), "=r"(v.y)
+                 : "l"(p), "l"(pol_first()));
+  }
   return v;
 }
-template <int HINT>
-__device__ __forceinline__ float4 ldB_h(const float4 *p) {
-  if (HINT < 2) return __ldg(p);
+// gathered source row: HINT 0 plain LDG; 2 evict_last; 3 evict_last for hot
+// rows, evict_first otherwise; COH: ld.global.cg (coherent at L2: rows that
+// peers store during the launch)
+template <int HINT, bool COH>
+__device__ __forceinline__ float4 ldB(const float4 *p, bool hot) {
   float4 v;
-  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "l"(p), "l"(pol_last()));
+  if (COH) {
+    asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p));
+  } else if (HINT == 0) {
+    v = __ldg(p);
+  } else {
+    const uint64_t pol = (HINT == 2 || hot) ? pol_last() : pol_first();
+    asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p), "l"(pol));
+  }
   return v;
 }
 template <int HINT>
@@ -95,58 +108,45 @@ __device__ __forceinline__ void add4(float4 &acc, const float4 &x) {
   acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
 }
 
-// Early READY of the fused exchange (SpmmArgs::sig_*): called by a whole lane
-// group after its peer-destined unit is stored.  Every lane fences its own
-// NVLink stores at system scope before lane 0 counts the unit; the lane group
-// that counts the last unit fences again (fence-fence synchronisation through
-// the counter) and publishes READY with release semantics.
-__device__ __noinline__ void sig_unit_done(int32_t *ctr, int32_t target, const int32_t *epoch,
-                                          int32_t *const *ptrs, int32_t n, int li, unsigned mask) {
-  __threadfence_system();
-  __syncwarp(mask);
-  if (li == 0) {
-    const int d = atomicAdd(ctr, 1);
-    if (d == target - 1) {
-      __threadfence_system();
-      const int32_t v = *epoch + 1;
-      for (int i = 0; i < n; ++i)
-        asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(ptrs[i]), "r"(v) : "memory");
-      *ctr = 0;   // re-arm for the next launch
-    }
-  }
-  __syncwarp(mask);
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
-#define SHIRO_SIG_DONE(a, li, mask) \
-  sig_unit_done((a).sig_ctr, (a).sig_target, (a).sig_epoch, (a).sig_ptrs, (a).sig_n, li, mask)
 
-// In-kernel READY wait of the consumer (SpmmArgs::wait_*), whole warp.
-__device__ __noinline__ bool wait_flags_ready(const int32_t *flags, int32_t n,
-                                              const int32_t *epoch, int32_t *err,
-                                              int64_t timeout_ns, int lane) {
-  const int32_t value = *epoch;
-  uint64_t t0;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+// Per-source READY wait of one warp (SpmmArgs::ready): bit s of `need` set ->
+// wait until ready[s] >= target.  Lane s polls source s (P <= 64: two
+// rounds).  Gives up at the warp's own timeout or as soon as another warp
+// has raised *err (one timeout in total, however many waves the grid has).
+__device__ __noinline__ bool wait_sources(const int32_t *ready, uint64_t need, int32_t target,
+                                          int32_t *err, int64_t timeout_ns, int lane) {
+  const uint64_t t0 = gtimer();
   for (;;) {
     bool ok = true;
-    for (int i = lane; i < n; i += 32) {
-      int32_t v;
-      asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(flags + i) : "memory");
-      ok = ok && v >= value;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int s = lane + 32 * h;
+      if ((need >> s) & 1ull) {
+        int32_t v;
+        asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(ready + s) : "memory");
+        ok = ok && v >= target;
+      }
     }
-    if (__all_sync(0xffffffffu, ok)) return true;
-    uint64_t t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    if ((int64_t)(t - t0) > timeout_ns) {
+    if (__all_sync(0xffffffffu, ok)) break;
+    if (*reinterpret_cast<volatile int32_t *>(err)) return false;
+    if ((int64_t)(gtimer() - t0) > timeout_ns) {
       if (lane == 0) atomicExch(err, 1);
       return false;
     }
-    __nanosleep(256);
+    __nanosleep(128);
   }
+  __syncwarp();   // order every lane's source loads after the acquiring lanes
+  return true;
 }
 
 // Output row address of a pointer-routed row: a peer (or own) buffer address,
 // or -- top bit set -- a row index into Y (the caller's C: local rows of the
-// fused producer launch, whose address is only known at call time).
+// hierarchical Stage-I launch, whose address is only known at call time).
 __device__ __forceinline__ float4 *out_addr(const SpmmArgs &a, long long v) {
   if (v < 0) return reinterpret_cast<float4 *>(a.Y + (v & 0x7fffffffffffffffLL) * a.N);
   return reinterpret_cast<float4 *>(v);
@@ -161,7 +161,7 @@ __device__ __forceinline__ const float4 *src_row(const SpmmArgs &a, int c) {
 
 // Gather U source rows for nonzeros j..j+U-1 of the current batch; the
 // weights are broadcast together with the columns, before any FMA.
-template <int LPR, int VPL, bool TWO, int U, int HINT = 0>
+template <int LPR, int VPL, bool TWO, int U, int HINT, bool COH>
 __device__ __forceinline__ void gather(const SpmmArgs &a, float4 (&x)[U][VPL], float (&w)[U],
                                        int c, float v, int j, int cnt, int li, unsigned mask) {
 #pragma unroll
@@ -169,9 +169,9 @@ __device__ __forceinline__ void gather(const SpmmArgs &a, float4 (&x)[U][VPL], f
     const int cu = __shfl_sync(mask, c, j + u, LPR);
     const float vu = __shfl_sync(mask, v, j + u, LPR);
     if (j + u < cnt) {               // uniform across the lane group
-      const float4 *r = src_row<TWO>(a, cu);
+      const float4 *r = src_row<TWO>(a, cu & 0x7fffffff);
 #pragma unroll
-      for (int q = 0; q < VPL; ++q) x[u][q] = ldB_h<HINT>(r + li + q * LPR);
+      for (int q = 0; q < VPL; ++q) x[u][q] = ldB<HINT, COH>(r + li + q * LPR, cu < 0);
       w[u] = vu;
     } else {
 #pragma unroll
@@ -184,7 +184,7 @@ __device__ __forceinline__ void gather(const SpmmArgs &a, float4 (&x)[U][VPL], f
 // One work unit u: a chunk task (u < n_tasks) or a row group.  OUTP: output
 // rows are addressed by a per-row pointer (e.g. a peer's receive buffer over
 // NVLink, the fused exchange) instead of Y + out_row * N.
-template <int LPR, int VPL, bool ACCUM, bool TWO, int U, bool OUTP, int HINT = 0>
+template <int LPR, int VPL, bool ACCUM, bool TWO, int U, bool OUTP, int HINT, bool COH>
 __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, const int li,
                                           const unsigned mask) {
   float4 acc[VPL];
@@ -208,7 +208,7 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
       for (int j = 0; j < cnt; j += U) {
         float4 x[U][VPL];
         float w[U];
-        gather<LPR, VPL, TWO, U, HINT>(a, x, w, cv.x, __int_as_float(cv.y), j, cnt, li, mask);
+        gather<LPR, VPL, TWO, U, HINT, COH>(a, x, w, cv.x, __int_as_float(cv.y), j, cnt, li, mask);
 #pragma unroll
         for (int uu = 0; uu < U; ++uu)
 #pragma unroll
@@ -256,7 +256,6 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
         y[li + q * LPR] = s[q];
       }
       if (li == 0) a.long_counter[lr] = 0;    // re-arm for the next launch
-      if (OUTP && a.sig_ptrs && t < a.sig_rows) SHIRO_SIG_DONE(a, li, mask);
     }
     return;
   }
@@ -313,7 +312,7 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
     for (int j = 0; j < cnt; j += U) {
       float4 x[U][VPL];
       float w[U];
-      gather<LPR, VPL, TWO, U, HINT>(a, x, w, cv.x, __int_as_float(cv.y), j, cnt, li, mask);
+      gather<LPR, VPL, TWO, U, HINT, COH>(a, x, w, cv.x, __int_as_float(cv.y), j, cnt, li, mask);
 #pragma unroll
       for (int uu = 0; uu < U; ++uu) {
         const int rou = __shfl_sync(mask, ro, j + uu, LPR);
@@ -326,22 +325,48 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
     }
   }
   while (cur < nrows) flush();              // last row and trailing empty rows
-  if (OUTP && a.sig_ptrs && g.r0 < a.sig_rows) SHIRO_SIG_DONE(a, li, mask);
 }
 
-template <int LPR, int VPL, bool ACCUM, bool TWO, int MINB, int U, bool OUTP, int BS = kBlock,
-          int HINT = 0>
+// N <= 128 (VPL = 1): one-warp CTAs (BS = 32), 32 resident per SM; wider
+// rows (VPL > 1) keep 8-warp CTAs without a residency floor (no spills).
+template <int LPR, int VPL, bool ACCUM, bool TWO, int U, bool OUTP, int HINT, bool WAIT,
+          int BS = 32, int MINB = 32>
 __global__ void __launch_bounds__(BS, MINB) k_spmm(const SpmmArgs a) {
   constexpr int R = 32 / LPR;   // lane groups per warp
   const int lane = threadIdx.x & 31;
   const int sub = lane / LPR;
   const int li = lane % LPR;
   const unsigned mask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (sub * LPR));
-  const int64_t warp = ((int64_t)blockIdx.x * BS + threadIdx.x) >> 5;
-  if (ACCUM && a.wait_flags &&
-      !wait_flags_ready(a.wait_flags, a.wait_n, a.wait_epoch, a.wait_err, a.wait_timeout_ns, lane))
+  const int64_t u = (((int64_t)blockIdx.x * BS + threadIdx.x) >> 5) * R + sub;
+  if (WAIT) {
+    // target epoch read before this warp is counted done (the last warp
+    // advances it, after every warp has read it)
+    const int32_t target = *reinterpret_cast<volatile int32_t *>(a.wait_epoch) + 1;
+    const int64_t units = (int64_t)a.n_tasks + a.n_groups;
+    uint64_t need = (u < units && li == 0) ? a.unit_src[u] : 0ull;
+    // union over the warp's lane groups
+    for (int o = 16; o > 0; o >>= 1) need |= __shfl_xor_sync(0xffffffffu, need, o);
+    const bool ok = wait_sources(a.ready, need, target, a.wait_err, a.wait_timeout_ns, lane);
+    if (ok) spmm_unit<LPR, VPL, ACCUM, TWO, (U < LPR ? U : LPR), OUTP, HINT, true>(a, u, li, mask);
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) {
+      __threadfence();
+      last = atomicAdd(a.done_ctr, 1) == (int)(gridDim.x * (BS / 32)) - 1;
+    }
+    if (__shfl_sync(0xffffffffu, last, 0)) {
+      // step-end barrier: READY from every peer, also those this rank reads nothing from
+      const uint64_t all = a.wait_all >= 64 ? ~0ull : ((1ull << a.wait_all) - 1ull);
+      wait_sources(a.ready, all, target, a.wait_err, a.wait_timeout_ns, lane);
+      if (lane == 0) {
+        *a.done_ctr = 0;
+        __threadfence();
+        *reinterpret_cast<volatile int32_t *>(a.wait_epoch) = target;
+      }
+    }
     return;
-  spmm_unit<LPR, VPL, ACCUM, TWO, (U < LPR ? U : LPR), OUTP, HINT>(a, warp * R + sub, li, mask);
+  }
+  spmm_unit<LPR, VPL, ACCUM, TWO, (U < LPR ? U : LPR), OUTP, HINT, false>(a, u, li, mask);
 }
 
 // Generic width (N not a supported vector width): one warp per CSR row,
@@ -364,13 +389,13 @@ __global__ void __launch_bounds__(kBlock) k_spmm_generic(const SpmmArgs a) {
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
     for (int64_t k = kb; k < ke; ++k) {
       const int2 cv = a.cv[k];
-      const int c = cv.x;
+      const int c = cv.x & 0x7fffffff;
       const float v = __int_as_float(cv.y);
       const float *r = (c < a.n0) ? a.X0 + (int64_t)c * a.N : a.X1 + (int64_t)(c - a.n0) * a.N;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int x = c0 + lane + 32 * q;
-        if (x < a.N) acc[q] = fmaf(v, __ldg(r + x), acc[q]);
+        if (x < a.N) acc[q] = fmaf(v, __ldcg(r + x), acc[q]);
       }
     }
 #pragma unroll
@@ -412,6 +437,8 @@ __global__ void __launch_bounds__(kBlock) k_pack(int64_t n, const int32_t *__res
 }
 
 // K4 into peer buffers: Y row of packed row i is the pointer dstp[i].
+// The source may be a buffer peers store into during other launches (the
+// hierarchical forward reads its own R1), so it is read L2-coherently.
 template <int LPR, int VPL>
 __global__ void __launch_bounds__(kBlock) k_pack_ptr(int64_t n, const int32_t *__restrict__ src,
                                                      float *const *__restrict__ dstp,
@@ -428,7 +455,7 @@ __global__ void __launch_bounds__(kBlock) k_pack_ptr(int64_t n, const int32_t *_
     if (u0 + r < n) {
       const float4 *s = reinterpret_cast<const float4 *>(X + (int64_t)__ldg(src + u0 + r) * N);
 #pragma unroll
-      for (int q = 0; q < VPL; ++q) x[r][q] = __ldg(s + li + q * LPR);
+      for (int q = 0; q < VPL; ++q) x[r][q] = __ldcg(s + li + q * LPR);
     }
   }
 #pragma unroll
@@ -449,7 +476,7 @@ __global__ void __launch_bounds__(kBlock) k_pack_ptr_generic(int64_t n, const in
   if (u >= n) return;
   const float *s = X + (int64_t)src[u] * N;
   float *d = dstp[u];
-  for (int x = lane; x < N; x += 32) d[x] = s[x];
+  for (int x = lane; x < N; x += 32) d[x] = __ldcg(s + x);
 }
 
 __global__ void __launch_bounds__(kBlock) k_pack_generic(int64_t n, const int32_t *src,
@@ -520,92 +547,59 @@ __global__ void __launch_bounds__(kBlock) k_scatter_add_generic(int64_t nt, cons
   }
 }
 
+__global__ void k_refresh(int64_t nnz, const int32_t *__restrict__ vsrc,
+                          const float *__restrict__ V, int2 *__restrict__ cv) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t s = vsrc[k];
+    if (s >= 0) cv[k].y = __float_as_int(V[s]);
+  }
+}
+
 inline int64_t blocks_for(int64_t units, int rows_per_warp) {
   const int64_t per_block = (int64_t)(kBlock / 32) * rows_per_warp;
   return (units + per_block - 1) / per_block;
 }
 
-template <int LPR, int VPL, int MINB, int U, int BS = kBlock, int H = 0>
+template <int LPR, int VPL, int H>
 void spmm_launch(const SpmmArgs &a, bool acc, cudaStream_t s) {
+  constexpr int U = VPL == 1 ? 4 : 8;
+  constexpr int BS = VPL == 1 ? 32 : 256, MINB = VPL == 1 ? 32 : 1;
   const int64_t units = a.n_tasks + a.n_groups;
-  const int64_t per_block = (int64_t)(BS / 32) * (32 / LPR);
-  const unsigned grid = (unsigned)((units + per_block - 1) / per_block);
+  const int64_t per_cta = (int64_t)(BS / 32) * (32 / LPR);
+  const unsigned grid = (unsigned)((units + per_cta - 1) / per_cta);
   const bool two = a.X1 != nullptr;
-  if (a.out_ptr) {   // fused exchange: overwrite rows in peer buffers
-    k_spmm<LPR, VPL, false, false, MINB, U, true, BS, H><<<grid, BS, 0, s>>>(a);
+  if (a.ready) {     // fused-exchange consumer: per-source waits, coherent source loads
+    k_spmm<LPR, VPL, true, false, U, false, 0, true, BS, MINB><<<grid, BS, 0, s>>>(a);
+  } else if (a.out_ptr) {   // fused exchange: overwrite rows in peer buffers
+    k_spmm<LPR, VPL, false, false, U, true, H, false, BS, MINB><<<grid, BS, 0, s>>>(a);
   } else if (acc) {
-    if (two) k_spmm<LPR, VPL, true, true, MINB, U, false, BS, H><<<grid, BS, 0, s>>>(a);
-    else k_spmm<LPR, VPL, true, false, MINB, U, false, BS, H><<<grid, BS, 0, s>>>(a);
+    if (two) k_spmm<LPR, VPL, true, true, U, false, H, false, BS, MINB><<<grid, BS, 0, s>>>(a);
+    else k_spmm<LPR, VPL, true, false, U, false, H, false, BS, MINB><<<grid, BS, 0, s>>>(a);
   } else {
-    if (two) k_spmm<LPR, VPL, false, true, MINB, U, false, BS, H><<<grid, BS, 0, s>>>(a);
-    else k_spmm<LPR, VPL, false, false, MINB, U, false, BS, H><<<grid, BS, 0, s>>>(a);
+    if (two) k_spmm<LPR, VPL, false, true, U, false, H, false, BS, MINB><<<grid, BS, 0, s>>>(a);
+    else k_spmm<LPR, VPL, false, false, U, false, H, false, BS, MINB><<<grid, BS, 0, s>>>(a);
   }
 }
 
-// Kernel variant: (resident CTAs per SM requested from ptxas, gather depth U).
-// SHIRO_KVAR selects one for tuning sweeps; the default is the measured best.
-int spmm_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char *e = getenv("SHIRO_KVAR");
-    v = e ? atoi(e) : 0;
-    if (const char *k = getenv("SHIRO_KERNEL")) {   // 4, 11..18: CTA-size variants of k_spmm
-      const int kk = atoi(k);
-      if (kk >= 11 || kk == 4) v = kk;
-    }
-  }
-  return v;
+// L2 policy of a launch (SHIRO_L2HINT overrides): 3 when the op carries hot
+// marks, 2 when its source rows fit comfortably in L2 (c2: B = 87 MB, -5 %),
+// else 0 (profiles/r1_kernel_sweep.txt, "L2 hints").
+int l2_hint(const SpmmArgs &a) {
+  static const int env_hint = getenv("SHIRO_L2HINT") ? atoi(getenv("SHIRO_L2HINT")) : -1;
+  if (env_hint >= 0) return (env_hint == 3 && !a.hot) ? 0 : env_hint;
+  if (a.hot) return 3;
+  return (a.X1 == nullptr && a.n0 * (int64_t)a.N * 4 <= (96ll << 20)) ? 2 : 0;
 }
 
 template <int LPR, int VPL>
 void spmm_shape(const SpmmArgs &a, bool acc, cudaStream_t s) {
-  if (VPL > 1) { spmm_launch<LPR, VPL, 1, 8>(a, acc, s); return; }
-#ifdef SHIRO_KERNEL_SWEEP   // tuning builds only (SHIRO_SWEEP=1 python -m ...build)
-  switch (spmm_variant()) {
-    case 1: spmm_launch<LPR, VPL, 3, 8>(a, acc, s); return;
-    case 3: spmm_launch<LPR, VPL, 4, 4>(a, acc, s); return;
-    case 5: spmm_launch<LPR, VPL, 6, 4>(a, acc, s); return;
-    case 6: spmm_launch<LPR, VPL, 1, 8>(a, acc, s); return;
-    case 7: spmm_launch<LPR, VPL, 5, 8>(a, acc, s); return;
-    case 8: spmm_launch<LPR, VPL, 6, 8>(a, acc, s); return;
-    case 2: spmm_launch<LPR, VPL, 4, 8>(a, acc, s); return;
-    default: break;
+  if constexpr (VPL == 1 && LPR >= 8) {
+    const int h = l2_hint(a);
+    if (h == 2) { spmm_launch<LPR, VPL, 2>(a, acc, s); return; }
+    if (h == 3) { spmm_launch<LPR, VPL, 3>(a, acc, s); return; }
   }
-#endif
-#ifdef SHIRO_KERNEL_SWEEP
-  switch (spmm_variant()) {   // CTA-size variants (profiles/r1_kernel_sweep.txt)
-    case 11: spmm_launch<LPR, VPL, 20, 4, 64>(a, acc, s); return;
-    case 12: spmm_launch<LPR, VPL, 10, 4, 128>(a, acc, s); return;
-    case 13: spmm_launch<LPR, VPL, 16, 8, 64>(a, acc, s); return;
-    case 15: spmm_launch<LPR, VPL, 32, 8, 32>(a, acc, s); return;
-    case 16: spmm_launch<LPR, VPL, 16, 4, 64>(a, acc, s); return;
-    case 17: spmm_launch<LPR, VPL, 24, 8, 32>(a, acc, s); return;
-    case 18: spmm_launch<LPR, VPL, 24, 4, 32>(a, acc, s); return;
-    default: break;
-  }
-#endif
-  if (spmm_variant() == 4) {   // round-1 baseline: 8-warp CTAs, 48 regs (SHIRO_KERNEL=4)
-    spmm_launch<LPR, VPL, 5, 4>(a, acc, s);
-    return;
-  }
-  // measured best (profiles/r1_kernel_sweep.txt): one-warp CTAs, 32 per SM
-  // (the per-SM CTA limit), 64 registers without spills.  A CTA retires as
-  // soon as its single unit is done, so power-law unit lengths no longer
-  // leave finished warps idle inside a CTA (8-warp CTAs: 42 % achieved vs
-  // 62 % theoretical occupancy on c2), and the spills of the 48-register
-  // build are gone: -17..19 % on c2/c3/c4.
-  // L2 policy (profiles/r1_kernel_sweep.txt, "L2 hints"): when the source
-  // rows fit comfortably in L2 (c2: 87 MB) the streams (A, C) go evict_first
-  // and the gathered rows evict_last (c2 -5 %); for sources far larger than
-  // L2 (c3/c4) the hints measured neutral to +0.5 %, so none.
-  static const int env_hint = getenv("SHIRO_L2HINT") ? atoi(getenv("SHIRO_L2HINT")) : -1;
-  const int hint = env_hint >= 0 ? env_hint
-                                 : ((a.X1 == nullptr && a.n0 * (int64_t)a.N * 4 <= (96ll << 20)) ? 2 : 0);
-  if constexpr (LPR == 32 && VPL == 1) {
-    if (hint == 1) { spmm_launch<LPR, VPL, 32, 4, 32, 1>(a, acc, s); return; }
-    if (hint == 2) { spmm_launch<LPR, VPL, 32, 4, 32, 2>(a, acc, s); return; }
-  }
-  spmm_launch<LPR, VPL, 32, 4, 32>(a, acc, s);
+  spmm_launch<LPR, VPL, 0>(a, acc, s);
 }
 
 template <int LPR, int VPL>
@@ -643,119 +637,7 @@ void scatter_shape(int64_t nt, const int32_t *tgt, const int64_t *ptr, const int
     else FN<32, 4>(__VA_ARGS__);                          \
   } while (0)
 
-// ---------------------------------------------------------------------------
-// Fused step kernel: compute -> NVLink exchange -> compute in ONE launch.
-// Persistent lane groups pull producer units (K4 pack rows, K3 partial rows
-// stored into the peers' receive buffers, K1 local rows into C) from a
-// counter; the lane group completing the last producer unit raises READY at
-// every peer (after every unit's stores were fenced at system scope).  Lane
-// groups that run out of producer work wait until every peer's READY and
-// this GPU's own producer count are complete, then pull remote units (K2 +
-// K5 fused, accumulating into C).  Producer units are all claimed by running
-// lane groups before anyone waits, so non-resident CTAs cannot deadlock the
-// step; waits time out into an error flag instead of hanging the GPU.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void st_release_sys_i32(int32_t *p, int32_t v) {
-  asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ int32_t ld_acquire_sys_i32(const int32_t *p) {
-  int32_t v;
-  asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ int32_t ld_acquire_gpu_i32(const int32_t *p) {
-  int32_t v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ uint64_t gtimer() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-
-template <int LPR, int VPL, int MINB, int U>
-__global__ void __launch_bounds__(kBlock, MINB) k_step(const StepArgs s) {
-  const int lane = threadIdx.x & 31;
-  const int sub = lane / LPR;
-  const int li = lane % LPR;
-  const unsigned mask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (sub * LPR));
-  const int totA = s.prod.n_tasks + s.prod.n_groups;
-  const int totB = s.rem.n_tasks + s.rem.n_groups;
-  const int32_t e = *s.epoch + 1;
-  auto signal_ready = [&]() {
-    __threadfence_system();
-    for (int i = li; i < s.n_peers; i += LPR) st_release_sys_i32(s.ready_ptrs[i], e);
-  };
-  // ---- phase A: producer units, static grid-stride assignment ---------------
-  const int R = 32 / LPR;
-  const int64_t nlg = (int64_t)gridDim.x * (kBlock / 32) * R;          // lane groups
-  const int64_t lg = (((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5) * R + sub;
-  for (int64_t u = lg; u < totA; u += nlg)
-    spmm_unit<LPR, VPL, false, false, (U < LPR ? U : LPR), true>(s.prod, u, li, mask);
-  // one system-scope fence + one completion count per lane group; the last
-  // lane group raises READY at every peer
-  __threadfence_system();
-  __syncwarp(mask);
-  {
-    int done = 0;
-    if (li == 0) done = atomicAdd(s.ctr + 1, 1);
-    done = __shfl_sync(mask, done, 0, LPR);
-    if (done == nlg - 1) signal_ready();
-  }
-  // ---- wait: own producers complete, every peer READY ----------------------
-  {
-    const uint64_t t0 = gtimer();
-    bool ok = true;
-    for (;;) {
-      bool ready = ld_acquire_gpu_i32(s.ctr + 1) >= nlg;
-      for (int i = li; i < s.P && ready; i += LPR) ready = ld_acquire_sys_i32(s.ready_local + i) >= e;
-      ready = __all_sync(mask, ready);
-      if (ready) break;
-      if ((int64_t)(gtimer() - t0) > s.timeout_ns) { ok = false; break; }
-      __nanosleep(128);
-    }
-    if (!ok) {
-      if (li == 0) atomicExch(s.err, 1);
-      return;
-    }
-  }
-  // ---- phase B: remote units (accumulate), static grid-stride --------------
-  for (int64_t u = lg; u < totB; u += nlg)
-    spmm_unit<LPR, VPL, true, false, (U < LPR ? U : LPR), false>(s.rem, u, li, mask);
-}
-
-template <int LPR, int VPL>
-void step_shape(const StepArgs &s, cudaStream_t st) {
-  static int per_sm = 0;
-  if (!per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step<LPR, VPL, 5, 4>, kBlock, 0);
-    if (per_sm < 1) per_sm = 1;
-  }
-  const int64_t unitsA = s.prod.n_tasks + s.prod.n_groups, unitsB = s.rem.n_tasks + s.rem.n_groups;
-  const int64_t need = blocks_for(std::max<int64_t>(std::max(unitsA, unitsB), 1), 32 / LPR);
-  const int64_t grid = std::min<int64_t>((int64_t)per_sm * num_sms(), need);
-  // cooperative launch: every CTA co-resident (lane groups wait on each other)
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(kBlock);
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_step<LPR, VPL, 5, 4>, s);
-}
-
 }  // namespace
-
-int launch_step(const StepArgs &s, cudaStream_t st) {
-  int lpr, vpl;
-  if (!vec_shape(s.prod.N, &lpr, &vpl) || vpl != 1) return -1;   // caller falls back
-  SHIRO_DISPATCH(s.prod.N, step_shape, s, st);
-  return 1;
-}
 
 // Vector shape for width N: LPR lanes per row, VPL float4 per lane.
 bool vec_shape(int N, int *lpr, int *vpl) {
@@ -788,7 +670,6 @@ int launch_spmm(const SpmmArgs &a, bool accumulate, cudaStream_t s) {
   int lpr, vpl;
   if (vec_shape(a.N, &lpr, &vpl)) {
     if (a.n_tasks + a.n_groups == 0) return 0;
-    if (vpl == 1 && launch_spmm2(a, accumulate, s)) return 1;   // pipelined kernel (spmm2.cu)
     SHIRO_DISPATCH(a.N, spmm_shape, a, accumulate, s);
   } else {
     const int64_t grid = blocks_for(a.nrows, 1);
@@ -834,6 +715,14 @@ int launch_scatter_add(int64_t nt, const int32_t *tgt, const int64_t *ptr, const
     k_scatter_add_generic<<<(unsigned)blocks_for(nt, 1), kBlock, 0, s>>>(nt, tgt, ptr, src, R, C,
                                                                           N);
   }
+  return 1;
+}
+
+int launch_refresh(int64_t nnz, const int32_t *vsrc, const float *V, int2 *cv, cudaStream_t s) {
+  if (nnz == 0) return 0;
+  const int64_t want = (nnz + 255) / 256;
+  const unsigned grid = (unsigned)std::min<int64_t>(want, (int64_t)num_sms() * 8);
+  k_refresh<<<grid, 256, 0, s>>>(nnz, vsrc, V, cv);
   return 1;
 }
 

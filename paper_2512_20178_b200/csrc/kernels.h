@@ -8,23 +8,28 @@ namespace shiro {
 // One CSR SpMM launch (K1/K2/K3 of DESIGN.md):
 //   Y[out_row[t]] (+)= sum_{k in [rp[t], rp[t+1])} val[k] * X(col[k])
 // with X(c) = X0[c] for c < n0 and X1[c - n0] otherwise (unified source row
-// space, e.g. [B_local || receive buffer]).  val == nullptr means all ones.
-// out_row == nullptr means out_row[t] = t.  Rows with more than L nonzeros
-// are split into chunk tasks of L nonzeros (power-law hub rows); the chunk
-// partials are reduced in a fixed order by the last-arriving chunk, so the
-// result is deterministic.  All other rows are packed into row groups of at
-// most ~L nonzeros (plan time); one lane group streams a whole group, so the
-// gathers of consecutive short rows are in flight together.
+// space, e.g. [B_local || receive buffer]).  out_row == nullptr means
+// out_row[t] = t.  Rows with more than L nonzeros are split into chunk tasks
+// (power-law hub rows); the chunk partials are reduced in a fixed order by the
+// last-arriving chunk, so the result is deterministic.  All other rows are
+// packed into row groups of at most ~L nonzeros (plan time); one lane group
+// streams a whole group, so the gathers of consecutive short rows are in
+// flight together.
 // A row group: consecutive short rows [r0, r1) whose nonzeros are [k0, k1).
 struct RowGroup {
   int64_t k0, k1;
   int32_t r0, r1;
 };
 
+// Bit 31 of a column id in `cv` marks a "hot" source row (one of the most
+// referenced rows of the op, chosen at plan time): with the hot/cold L2
+// policy its gathers are L2 evict_last and the other gathers evict_first.
+constexpr int32_t kHotBit = (int32_t)0x80000000u;
+
 struct SpmmArgs {
   int64_t nrows = 0;
   const int64_t *rp = nullptr;          // [nrows+1]
-  const int2 *cv = nullptr;             // [nnz] interleaved (column, value bits)
+  const int2 *cv = nullptr;             // [nnz] interleaved (column [| kHotBit], value bits)
   const uint8_t *roff = nullptr;        // [nnz] row offset inside its row group
   const int32_t *out_row = nullptr;
   float *const *out_ptr = nullptr;      // per-row output address (fused exchange)
@@ -42,53 +47,34 @@ struct SpmmArgs {
   const int32_t *long_first = nullptr;  // [n_long+1] first task of each long row
   int32_t *long_counter = nullptr;      // [n_long] zero-initialised arrival counters
   float *scratch = nullptr;             // [n_tasks * N] chunk partials
-  // Early READY (fused exchange producer): rows [0, sig_rows) go to peers.
-  // When the last of their sig_target units (row groups + hub rows) has been
-  // stored, the lane group finishing it raises READY = *sig_epoch + 1 at the
-  // sig_n peer flags sig_ptrs[] (after system-scope fences), while the
-  // launch's local rows are still being computed.  sig_ptrs == nullptr: off.
-  int64_t sig_rows = 0;
-  int32_t sig_target = 0;
-  int32_t sig_n = 0;
-  int32_t *sig_ctr = nullptr;           // zero-initialised, re-armed by the signaller
-  int32_t *const *sig_ptrs = nullptr;
-  const int32_t *sig_epoch = nullptr;
-  // In-kernel wait (fused exchange consumer): before its unit, every warp
-  // spins until wait_flags[0..wait_n) >= *wait_epoch (ld.acquire.sys), with a
-  // %globaltimer timeout that sets *wait_err instead of hanging.  nullptr: off.
-  const int32_t *wait_flags = nullptr;
-  int32_t wait_n = 0;
-  const int32_t *wait_epoch = nullptr;
+  int32_t hot = 0;                      // 1: cv carries kHotBit marks (hot/cold L2 policy)
+  // Per-source wait (fused exchange consumer): unit u reads
+  // receive-buffer rows of the sources in unit_src[u] (bit s = source rank
+  // s); before it, its warp spins until ready[s] >= *wait_epoch + 1 for
+  // those sources only (ld.acquire.sys), so rows of a peer are consumed as
+  // soon as that peer's READY lands.  Source rows are then read with
+  // L2-coherent loads (the buffer is written by peers during the launch).
+  // A timeout (per warp, %globaltimer) or an error raised by any other warp
+  // sets / sees *wait_err and skips the unit instead of hanging the GPU.
+  // The last warp to finish first waits for EVERY source 0..wait_all-1 (the
+  // step-end barrier of the double-buffered exchange), then advances
+  // *wait_epoch (done_ctr re-armed).  ready == nullptr: off.
+  const int32_t *ready = nullptr;       // [P] local READY flags (one per source)
+  const uint64_t *unit_src = nullptr;   // [n_tasks + n_groups] source masks
+  int32_t *wait_epoch = nullptr;
   int32_t *wait_err = nullptr;
+  int32_t *done_ctr = nullptr;          // zero-initialised
+  int32_t wait_all = 0;                 // P (the last warp's barrier)
   int64_t wait_timeout_ns = 0;
 };
 
 // accumulate: false -> Y = A*X (overwrite, empty rows get zeros); true -> Y += A*X
 // returns the number of kernel launches issued (0 if nothing to do)
 int launch_spmm(const SpmmArgs &a, bool accumulate, cudaStream_t s);
-// software-pipelined variant for N in {32, 64, 128} (spmm2.cu); 0 = not
-// applicable (or SHIRO_KERNEL=1 selects the original k_spmm)
-int launch_spmm2(const SpmmArgs &a, bool accumulate, cudaStream_t s);
 
 // K4: Y[dst[i]] = X[src[i]] for i < n (gather B rows into the send buffer)
 int launch_pack(int64_t n, const int32_t *src, const int32_t *dst, const float *X, float *Y,
                 int32_t N, cudaStream_t s);
-
-// Fused step (one launch): producer op (pointer-routed, overwrite) -> READY
-// to peers -> wait for peers -> remote op (accumulate into C).
-struct StepArgs {
-  SpmmArgs prod, rem;
-  int *ctr = nullptr;                   // [3] zeroed before the launch
-  int32_t *const *ready_ptrs = nullptr; // peers' READY flags for this rank
-  int n_peers = 0;
-  const int32_t *ready_local = nullptr; // [P] READY flags of this rank
-  int P = 0;
-  const int32_t *epoch = nullptr;       // device epoch (value e-1)
-  int32_t *err = nullptr;
-  int64_t timeout_ns = 0;
-};
-// returns launches issued, or -1 if the width has no fused-step shape
-int launch_step(const StepArgs &s, cudaStream_t st);
 
 // K4 into peer memory: dstp[i] is the (peer-mapped) address of packed row i
 int launch_pack_ptr(int64_t n, const int32_t *src, float *const *dstp, const float *X, int32_t N,
@@ -97,8 +83,9 @@ int launch_pack_ptr(int64_t n, const int32_t *src, float *const *dstp, const flo
 // Fused-exchange synchronisation over NVLink (p2p.cu), value = *epoch + add
 // read on the device.  signal: for each i, st.release.sys *flags[i] = value
 // (flags[i] may be a peer address); bump: then *epoch = value.  wait: spin
-// until every local flags[i] >= value (ld.acquire.sys); after timeout_ns sets
-// *err = 1 and gives up instead of hanging the GPU.
+// until every local flags[i] >= value (ld.acquire.sys); after timeout_ns (or
+// as soon as *err is set by another waiter) sets *err = 1 and gives up
+// instead of hanging the GPU.
 int launch_signal(int32_t *const *flags, int n, int32_t *epoch, int add, bool bump,
                   cudaStream_t s);
 int launch_wait(const int32_t *flags, int n, int32_t *epoch, int add, int32_t *err,
@@ -108,6 +95,10 @@ int launch_wait(const int32_t *flags, int n, int32_t *epoch, int add, int32_t *e
 // received partial C rows, fixed order: C first, then sources ascending)
 int launch_scatter_add(int64_t nt, const int32_t *tgt, const int64_t *ptr, const int32_t *src,
                        const float *R, float *C, int32_t N, cudaStream_t s);
+
+// N3 value refresh: cv[k].y = bits(V[vsrc[k]]) for every k < nnz with
+// vsrc[k] >= 0 (a fixed pattern's device op takes new values in place).
+int launch_refresh(int64_t nnz, const int32_t *vsrc, const float *V, int2 *cv, cudaStream_t s);
 
 // SM count of the current device (cached)
 int num_sms();

@@ -52,6 +52,7 @@ __global__ void k_wait(const int32_t *flags, int n, int32_t *epoch, int add, int
   if (i < n) {
     const uint64_t t0 = globaltimer();
     while (ld_acquire_sys(flags + i) < value) {
+      if (*reinterpret_cast<volatile int32_t *>(err)) break;   // another waiter timed out
       if ((int64_t)(globaltimer() - t0) > timeout_ns) {
         atomicExch(err, 1);
         break;

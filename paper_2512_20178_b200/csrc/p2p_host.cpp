@@ -42,6 +42,11 @@ void p2p_release(Plan &pl) {
   pl.prod_ops = nullptr;
   if (pl.err_host) cudaFreeHost(pl.err_host);
   pl.err_host = nullptr;
+  if (pl.s_hi) cudaStreamDestroy(pl.s_hi);
+  if (pl.ev_fork) cudaEventDestroy(pl.ev_fork);
+  if (pl.ev_join) cudaEventDestroy(pl.ev_join);
+  pl.s_hi = nullptr;
+  pl.ev_fork = pl.ev_join = nullptr;
   pl.p2p = false;
 }
 
@@ -90,13 +95,12 @@ void p2p_setup(Plan &pl, const Alltoallv &xchg) {
   auto peer_recv = [&](int d) {
     return reinterpret_cast<char *>(pl.peer_base[d]) + pm[d].recv_buf_off;
   };
-  // double buffering needs a second receive buffer on every rank (and not the
-  // opt-in single-launch step, which keeps the CONSUMED protocol)
+  // double buffering needs a second receive buffer on every rank; each rank
+  // sees every peer's choice (recv_buf2_off < 0 = none), so all ranks agree
+  // on the protocol even if SHIRO_DBUF differs between them
   bool dbuf = pl.recv_buf2_off >= 0;
   for (int d = 0; d < P; ++d)
     if (d != me && pm[d].recv_buf2_off < 0) dbuf = false;
-  if (const char *e = getenv("SHIRO_FUSED_STEP"))
-    if (e[0] == '1') dbuf = false;
   std::vector<uint64_t> dstp, outp, dstp2, outp2, rdy, cons;
   for (int d = 0; d < P; ++d) {
     if (d == me) continue;
@@ -119,16 +123,14 @@ void p2p_setup(Plan &pl, const Alltoallv &xchg) {
   }
   if ((int64_t)outp.size() != pl.d_out.a.nrows || (int64_t)dstp.size() != pl.d_pack.n)
     throw Error(SHIRO_E_INTERNAL, "fused exchange: row count mismatch");
-  // K4 + K3 + K1 as one pointer-routed launch (one destination table per buffer)
-  if (dbuf) upload_prod(pl, pl.pack_src, dstp, outp, &dstp2, &outp2);
-  else upload_prod(pl, pl.pack_src, dstp, outp);
+  // K4 + K3 as one pointer-routed launch (one destination table per buffer)
+  if (dbuf) upload_prod(pl, pl.pack_src, dstp, outp, false, &dstp2, &outp2);
+  else upload_prod(pl, pl.pack_src, dstp, outp, false);
   pl.dbuf = dbuf;
   pl.step_parity = 0;
   const size_t n_all = rdy.size() + cons.size();
-  // pointer arrays, then 2 x uint64 of fused-step work counters
-  SHIRO_CK(cudaMalloc(&pl.p2p_arena, (n_all + 2) * sizeof(uint64_t)));
+  SHIRO_CK(cudaMalloc(&pl.p2p_arena, std::max<size_t>(1, n_all) * sizeof(uint64_t)));
   uint64_t *a = static_cast<uint64_t *>(pl.p2p_arena);
-  pl.step_ctr = reinterpret_cast<int *>(a + n_all);
   std::vector<uint64_t> all;
   all.insert(all.end(), rdy.begin(), rdy.end());
   all.insert(all.end(), cons.begin(), cons.end());
@@ -137,7 +139,7 @@ void p2p_setup(Plan &pl, const Alltoallv &xchg) {
   pl.ready_ptrs = reinterpret_cast<int32_t *const *>(a);
   pl.consumed_ptrs = reinterpret_cast<int32_t *const *>(a + rdy.size());
   // 5. local flags: own entries never block (INT_MAX), the rest start at 0
-  std::vector<int32_t> f(2 * P + 2, 0);
+  std::vector<int32_t> f(2 * P + 4, 0);
   f[me] = INT_MAX;
   f[P + me] = INT_MAX;
   SHIRO_CK(cudaMemcpy(pl.xflags, f.data(), f.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
@@ -145,6 +147,12 @@ void p2p_setup(Plan &pl, const Alltoallv &xchg) {
   *pl.err_host = 0;
   if (const char *e = getenv("SHIRO_P2P_TIMEOUT_MS")) pl.wait_timeout_ns = atoll(e) * 1000000LL;
   pl.epoch = 0;
+  // the producer branch of a step runs on a high-priority stream
+  int lo_prio = 0, hi_prio = 0;
+  SHIRO_CK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+  SHIRO_CK(cudaStreamCreateWithPriority(&pl.s_hi, cudaStreamNonBlocking, hi_prio));
+  SHIRO_CK(cudaEventCreateWithFlags(&pl.ev_fork, cudaEventDisableTiming));
+  SHIRO_CK(cudaEventCreateWithFlags(&pl.ev_join, cudaEventDisableTiming));
   pl.p2p = true;
   // every rank's flags are initialised before any peer signals into them
   std::vector<std::vector<char>> bar_send(P, bytes_of(0)), bar_recv;

@@ -126,6 +126,7 @@ Phase1 plan_phase1(const PlanInput &in) {
   p1.n_rows.assign(P, 0);
   p1.n_cols.assign(P, 0);
   p1.nnz_row.assign(P, 0);
+  p1.ship_idx.assign(P, {});
 
   // owner of every nonzero's column; per-block nonzero index lists (CSR order)
   std::vector<int32_t> q_of(nnz);
@@ -177,7 +178,16 @@ Phase1 plan_phase1(const PlanInput &in) {
     const int32_t nr = (int32_t)urow.size(), nc = (int32_t)ucol.size();
     std::vector<uint8_t> sel_r, sel_c;
     const bool joint = !mode_col && !mode_row && !mode_block;
-    if (joint) block_cover(nr, nc, ap, adj, colmax, sel_r, sel_c);
+    if (joint && in.w_row) {
+      // weighted covers (Eqs. 4-8): vertex weights of the
+      // block's rows (C rows of this rank) and columns (B rows of q)
+      std::vector<int64_t> wr(nr), wc(nc);
+      for (int32_t u = 0; u < nr; ++u) wr[u] = in.w_row[urow[u]];
+      for (int32_t v = 0; v < nc; ++v) wc[v] = in.w_col[ucol[v]];
+      block_cover_weighted(nr, nc, ap, adj, wr, wc, colmax, sel_r, sel_c);
+    } else if (joint) {
+      block_cover(nr, nc, ap, adj, colmax, sel_r, sel_c);
+    }
     // SHIRO_F_COVER_BALANCE (R18): near-minimum all-rows cover -> all rows
     bool all_rows = false;
     if (joint && (in.flags & SHIRO_F_COVER_BALANCE)) {
@@ -230,7 +240,7 @@ Phase1 plan_phase1(const PlanInput &in) {
     m.put(0);
     for (auto x : b_ids) m.put(x);
     for (auto x : c_ids) m.put(x);
-    std::vector<int64_t> cols_w, vals_w;
+    std::vector<int64_t> cols_w, vals_w, ship;
     for (int32_t u = 0; u < nr; ++u) {
       if (!row_used[u]) continue;
       int64_t c = 0;
@@ -238,6 +248,7 @@ Phase1 plan_phase1(const PlanInput &in) {
         const int64_t k = idx[b0 + e];
         if (p1.tag[k] != 1) continue;
         ++c;
+        ship.push_back(k);
         cols_w.push_back(in.col[k]);
         int32_t bits;
         std::memcpy(&bits, &in.val[k], 4);
@@ -253,6 +264,7 @@ Phase1 plan_phase1(const PlanInput &in) {
     p1.n_rows[q] = nr;
     p1.n_cols[q] = nc;
     p1.nnz_row[q] = nrow_nz;
+    p1.ship_idx[q] = std::move(ship);
   });
   // empty blocks still get an (empty) message so every peer can parse one
   for (int q = 0; q < P; ++q)
@@ -280,6 +292,12 @@ void plan_phase2(const PlanInput &in, Phase1 &p1, const std::vector<std::vector<
   std::vector<std::vector<int64_t>> out_counts(P), out_cols(P);
   std::vector<std::vector<float>> out_vals(P);
   int64_t nnz_computed = 0;
+  // value space of the refresh (N3): [local values || values received from
+  // each peer, peers ascending, message order]
+  pl.nnz_local = nnz;
+  pl.ship_idx = std::move(p1.ship_idx);
+  pl.recv_vals.assign(P, 0);
+  std::vector<int64_t> vbase(P + 1, nnz);
   for (int p = 0; p < P; ++p) {
     if (p == r) continue;
     const auto &b = in_msgs[p];
@@ -301,7 +319,11 @@ void plan_phase2(const PlanInput &in, Phase1 &p1, const std::vector<std::vector<
     for (auto x : pl.send_b[p])
       if (x < lo || x >= lo + M) throw Error(SHIRO_E_INTERNAL, "send_b id not owned");
     nnz_computed += nz;
+    pl.recv_vals[p] = nz;
   }
+  for (int p = 0; p < P; ++p) vbase[p + 1] = vbase[p] + pl.recv_vals[p];
+  pl.nnz_recv_vals = nnz_computed;
+  if (vbase[P] > 0x7fffffffLL) throw Error(SHIRO_E_ARG, "more than 2^31 values on one rank");
 
   // buffer layouts: per peer ascending, [B rows || C rows]
   pl.send_off.assign(P + 1, 0);
@@ -329,6 +351,7 @@ void plan_phase2(const PlanInput &in, Phase1 &p1, const std::vector<std::vector<
       for (int64_t e = 0; e < out_counts[d][k]; ++e, ++pos) {
         ao.col.push_back((int32_t)(out_cols[d][pos] - lo));
         ao.val.push_back(out_vals[d][pos]);
+        ao.vsrc.push_back((int32_t)(vbase[d] + pos));
       }
       ao.rp.push_back((int64_t)ao.col.size());
       ao.out_row.push_back((int32_t)(pl.send_off[d] + pl.send_b[d].size() + k));
@@ -347,6 +370,7 @@ void plan_phase2(const PlanInput &in, Phase1 &p1, const std::vector<std::vector<
       if (p1.tag[k] == 0) {
         ad.col.push_back((int32_t)(in.col[k] - lo));
         ad.val.push_back(in.val[k]);
+        ad.vsrc.push_back((int32_t)k);
       }
     ad.rp.push_back((int64_t)ad.col.size());
   }
@@ -363,6 +387,7 @@ void plan_phase2(const PlanInput &in, Phase1 &p1, const std::vector<std::vector<
   ac = HostCsr();
   std::vector<std::vector<int32_t>> colrow_cols(M);   // per local row: recv indices
   std::vector<std::vector<float>> colrow_vals(M);
+  std::vector<std::vector<int32_t>> colrow_k(M);
   for (int64_t t = 0; t < M; ++t) {
     int q = 0;
     for (int64_t k = in.row_ptr[t]; k < in.row_ptr[t + 1]; ++k) {
@@ -374,10 +399,12 @@ void plan_phase2(const PlanInput &in, Phase1 &p1, const std::vector<std::vector<
       if (itj == lb.end() || *itj != j) throw Error(SHIRO_E_INTERNAL, "col-based B row missing");
       colrow_cols[t].push_back((int32_t)(pl.recv_off[q] + (itj - lb.begin())));
       colrow_vals[t].push_back(in.val[k]);
+      colrow_k[t].push_back((int32_t)k);
     }
     if (!colrow_cols[t].empty()) {
       ac.col.insert(ac.col.end(), colrow_cols[t].begin(), colrow_cols[t].end());
       ac.val.insert(ac.val.end(), colrow_vals[t].begin(), colrow_vals[t].end());
+      ac.vsrc.insert(ac.vsrc.end(), colrow_k[t].begin(), colrow_k[t].end());
       ac.rp.push_back((int64_t)ac.col.size());
       ac.out_row.push_back((int32_t)t);
     }
@@ -409,11 +436,15 @@ void plan_phase2(const PlanInput &in, Phase1 &p1, const std::vector<std::vector<
     if (colrow_cols[t].empty() && part_src[t].empty()) continue;
     ar.col.insert(ar.col.end(), colrow_cols[t].begin(), colrow_cols[t].end());
     ar.val.insert(ar.val.end(), colrow_vals[t].begin(), colrow_vals[t].end());
-    for (auto x : part_src[t]) { ar.col.push_back(x); ar.val.push_back(1.0f); }
+    ar.vsrc.insert(ar.vsrc.end(), colrow_k[t].begin(), colrow_k[t].end());
+    for (auto x : part_src[t]) { ar.col.push_back(x); ar.val.push_back(1.0f); ar.vsrc.push_back(-1); }
     ar.rp.push_back((int64_t)ar.col.size());
     ar.out_row.push_back((int32_t)t);
   }
   ar.nrows = (int64_t)ar.out_row.size();
+  ar.src_bounds = pl.recv_off;     // receive-buffer segment of each source (per-unit waits)
+  ad.hot_rows = M;                 // local rows read B_local (hot/cold L2 marks)
+  ao.hot_rows = M;
 
   // local statistics
   shiro_info_t &I = pl.info;
@@ -537,32 +568,118 @@ std::vector<std::vector<char>> transpose_messages(const PlanInput &in) {
 
 void transpose_assemble(const PlanInput &in, const std::vector<std::vector<char>> &msgs,
                         std::vector<int64_t> &rp, std::vector<int32_t> &col,
-                        std::vector<float> &val) {
+                        std::vector<float> &val, std::vector<int64_t> *perm) {
   const int64_t lo = in.part[in.rank], M = in.part[in.rank + 1] - lo;
-  std::vector<std::vector<std::pair<int32_t, float>>> rows(M);
+  struct Ent { int32_t i; float v; int64_t src; };   // src: index over the messages in order
+  std::vector<std::vector<Ent>> rows(M);
+  int64_t gidx = 0;
   for (const auto &b : msgs) {
     const int64_t *w = reinterpret_cast<const int64_t *>(b.data());
     const int64_t n3 = (int64_t)b.size() / 24;
-    for (int64_t e = 0; e < n3; ++e) {
+    for (int64_t e = 0; e < n3; ++e, ++gidx) {
       const int64_t j = w[3 * e], i = w[3 * e + 1];
       const int32_t bits = (int32_t)w[3 * e + 2];
       float v;
       std::memcpy(&v, &bits, 4);
       if (j < lo || j >= lo + M) throw Error(SHIRO_E_INTERNAL, "transpose: misrouted entry");
-      rows[j - lo].push_back({(int32_t)i, v});
+      rows[j - lo].push_back({(int32_t)i, v, gidx});
     }
   }
   rp.assign(1, 0);
   col.clear();
   val.clear();
+  if (perm) perm->clear();
   for (int64_t t = 0; t < M; ++t) {
     std::sort(rows[t].begin(), rows[t].end(),
-              [](const std::pair<int32_t, float> &a, const std::pair<int32_t, float> &b) {
-                return a.first < b.first;
-              });
-    for (auto &e : rows[t]) { col.push_back(e.first); val.push_back(e.second); }
+              [](const Ent &a, const Ent &b) { return a.i < b.i; });
+    for (auto &e : rows[t]) {
+      col.push_back(e.i);
+      val.push_back(e.v);
+      if (perm) perm->push_back(e.src);
+    }
     rp.push_back((int64_t)col.size());
   }
+}
+
+// ---------------------------------------------------------------------------
+// Value refresh (the plan is "reused across
+// multiple SpMM operations with the same sparsity pattern"): the cover, lists
+// and device layouts stay; only values move.  Each rank ships the new values
+// of its row-based nonzeros to the column owner in the plan-time message
+// order (one all-to-allv of 4 B per row-based nonzero), and assembles
+// V = [own values || received values, peers ascending].  Transposed plans
+// first redistribute the values exactly as the plan-time transpose did.
+// ---------------------------------------------------------------------------
+std::vector<std::vector<char>> refresh_ship(const Plan &pl, const float *lv) {
+  std::vector<std::vector<char>> snd(pl.P);
+  for (int q = 0; q < pl.P; ++q) {
+    if (q == pl.rank) continue;
+    const auto &ix = pl.ship_idx[q];
+    snd[q].resize(ix.size() * 4);
+    float *f = reinterpret_cast<float *>(snd[q].data());
+    for (size_t e = 0; e < ix.size(); ++e) f[e] = lv[ix[e]];
+  }
+  return snd;
+}
+
+std::vector<float> refresh_assemble(const Plan &pl, const float *lv,
+                                    const std::vector<std::vector<char>> &rcv) {
+  std::vector<float> V;
+  V.reserve(pl.nnz_local + pl.nnz_recv_vals);
+  V.insert(V.end(), lv, lv + pl.nnz_local);
+  for (int p = 0; p < pl.P; ++p) {
+    if (p == pl.rank) continue;
+    if ((int64_t)rcv[p].size() != 4 * pl.recv_vals[p])
+      throw Error(SHIRO_E_INTERNAL, "refresh: value message size mismatch");
+    const float *f = reinterpret_cast<const float *>(rcv[p].data());
+    V.insert(V.end(), f, f + pl.recv_vals[p]);
+  }
+  return V;
+}
+
+std::vector<float> refresh_value_space(Plan &pl, const PlanInput &in, const float *val,
+                                       const Alltoallv &xchg) {
+  const int P = pl.P, r = pl.rank;
+  std::vector<float> local;
+  const float *lv = val;
+  if (pl.flags & SHIRO_F_TRANSPOSE) {
+    // the entries of this rank's rows of A, in transpose_messages order, to
+    // the owner of each column; the receiver places them with tperm
+    const int64_t lo = in.part[r], M = in.part[r + 1] - lo;
+    std::vector<std::vector<char>> snd(P), rcv;
+    std::vector<std::vector<float>> w(P);
+    for (int64_t t = 0; t < M; ++t)
+      for (int64_t k = in.row_ptr[t]; k < in.row_ptr[t + 1]; ++k) {
+        int q = 0;
+        while (in.part[q + 1] <= in.col[k]) ++q;
+        w[q].push_back(val[k]);
+      }
+    for (int q = 0; q < P; ++q) {
+      snd[q].resize(w[q].size() * 4);
+      if (!w[q].empty()) std::memcpy(snd[q].data(), w[q].data(), snd[q].size());
+    }
+    if (P > 1) xchg(snd, rcv);
+    rcv.resize(P);
+    rcv[r] = snd[r];
+    std::vector<float> cat;
+    for (int q = 0; q < P; ++q) {
+      const float *f = reinterpret_cast<const float *>(rcv[q].data());
+      cat.insert(cat.end(), f, f + rcv[q].size() / 4);
+    }
+    if ((int64_t)pl.tperm.size() != pl.nnz_local)
+      throw Error(SHIRO_E_INTERNAL, "refresh: transposed value count mismatch");
+    local.resize(pl.nnz_local);
+    for (int64_t x = 0; x < pl.nnz_local; ++x) {
+      if (pl.tperm[x] < 0 || pl.tperm[x] >= (int64_t)cat.size())
+        throw Error(SHIRO_E_INTERNAL, "refresh: transposed index out of range");
+      local[x] = cat[pl.tperm[x]];
+    }
+    lv = local.data();
+  }
+  std::vector<std::vector<char>> snd = refresh_ship(pl, lv), rcv;
+  if (P > 1) xchg(snd, rcv);
+  rcv.resize(P);
+  return refresh_assemble(pl, lv, rcv);
 }
 
 }  // namespace shiro

@@ -34,6 +34,7 @@ Plan::~Plan() {
     if (comm_stream) cudaStreamDestroy(comm_stream);
     if (arena) cudaFree(arena);
     if (stage) cudaFree(stage);
+    if (vspace) cudaFree(vspace);
     for (cudaEvent_t e : {ev_in, ev_comp, ev_out})
       if (e) cudaEventDestroy(e);
     if (h2d_s) cudaStreamDestroy(h2d_s);
@@ -96,7 +97,40 @@ struct SplitHost {
   std::vector<RowGroup> groups;
   std::vector<uint8_t> roff;
   std::vector<int2> cv;
+  std::vector<uint64_t> unit_src;   // per unit (tasks, then groups): source mask
+  bool hot = false;
 };
+
+int64_t env_mb(const char *name, int64_t dflt) {
+  const char *e = getenv(name);
+  return e ? atoll(e) : dflt;
+}
+
+// Hot/cold L2 marks (kHotBit): when an op's source rows are far larger than
+// L2, the most referenced source rows (column degree >= 2, highest first, up
+// to SHIRO_HOT_MB of rows) are marked so that their gathers are L2
+// evict_last and every other gather evict_first.
+void mark_hot(const HostCsr &c, int N, SplitHost &s) {
+  const int64_t rowb = (int64_t)N * 4;
+  const int64_t budget = env_mb("SHIRO_HOT_MB", 0) << 20;
+  const int64_t min_src = env_mb("SHIRO_HOT_MIN_MB", 96) << 20;
+  if (c.hot_rows <= 0 || budget <= 0 || c.hot_rows * rowb <= min_src || c.nnz() == 0) return;
+  std::vector<int32_t> deg(c.hot_rows, 0);
+  for (int32_t j : c.col)
+    if (j >= 0 && j < c.hot_rows) deg[j]++;
+  std::vector<int32_t> ids;
+  for (int32_t j = 0; j < (int32_t)c.hot_rows; ++j)
+    if (deg[j] >= 2) ids.push_back(j);
+  const size_t H = std::min<size_t>(ids.size(), (size_t)(budget / rowb));
+  std::partial_sort(ids.begin(), ids.begin() + H, ids.end(), [&](int32_t a, int32_t b) {
+    return deg[a] != deg[b] ? deg[a] > deg[b] : a < b;
+  });
+  std::vector<uint8_t> hot(c.hot_rows, 0);
+  for (size_t i = 0; i < H; ++i) hot[ids[i]] = 1;
+  for (int64_t k = 0; k < c.nnz(); ++k)
+    if (c.col[k] >= 0 && c.col[k] < c.hot_rows && hot[c.col[k]]) s.cv[k].x |= kHotBit;
+  s.hot = H > 0;
+}
 
 SplitHost make_split(const HostCsr &c, int N) {
   SplitHost s;
@@ -109,6 +143,7 @@ SplitHost make_split(const HostCsr &c, int N) {
   }
   int lpr, vpl;
   if (!vec_shape(N, &lpr, &vpl)) return s;   // generic path: row per warp
+  mark_hot(c, N, s);
   s.L = unit_size(c.nnz());
   s.roff.assign(c.nnz(), 0);
   const int64_t max_rows = (c.out_row.empty() && !c.ptr_rows) ? kMaxGroupRows
@@ -134,21 +169,46 @@ SplitHost make_split(const HostCsr &c, int N) {
     }
     const int64_t r0 = t;
     int64_t sum = 0;
-    while (t < c.nrows && deg(t) <= H && t - r0 < max_rows && (t == r0 || sum + deg(t) <= s.L) &&
-           (t == r0 || t != c.split_row)) {
+    while (t < c.nrows && deg(t) <= H && t - r0 < max_rows && (t == r0 || sum + deg(t) <= s.L)) {
       for (int64_t k = c.rp[t]; k < c.rp[t + 1]; ++k) s.roff[k] = (uint8_t)(t - r0);
       sum += deg(t);
       ++t;
     }
     s.groups.push_back(RowGroup{c.rp[r0], c.rp[t], (int32_t)r0, (int32_t)t});
   }
+  if (!c.src_bounds.empty()) {
+    // per-unit source masks (fused exchange consumer): the sources whose
+    // receive-buffer segments the unit's nonzeros read
+    const auto &b = c.src_bounds;
+    if (b.size() > 65) throw Error(SHIRO_E_INTERNAL, "source masks need P <= 64");
+    auto mask_of = [&](int64_t k0, int64_t k1) {
+      uint64_t m = 0;
+      for (int64_t k = k0; k < k1; ++k) {
+        const int64_t x = c.col[k];
+        const int src = (int)(std::upper_bound(b.begin(), b.end(), x) - b.begin()) - 1;
+        if (src < 0 || src >= (int)b.size() - 1) throw Error(SHIRO_E_INTERNAL, "source of column");
+        m |= 1ull << src;
+      }
+      return m;
+    };
+    for (size_t i = 0; i < s.task_long.size(); ++i) {
+      const int32_t lr = s.task_long[i];
+      const int64_t t0 = s.long_row[lr];
+      const int64_t f = s.long_first[lr], nch = s.long_first[lr + 1] - f;
+      const int64_t rb = c.rp[t0], re = c.rp[t0 + 1];
+      const int64_t clen = (re - rb + nch - 1) / nch;    // as in the kernel
+      const int64_t kb = rb + ((int64_t)i - f) * clen, ke = std::min(re, kb + clen);
+      s.unit_src.push_back(mask_of(kb, ke));
+    }
+    for (const RowGroup &g : s.groups) s.unit_src.push_back(mask_of(g.k0, g.k1));
+  }
   return s;
 }
 
 struct SpmmLayout {
-  size_t rp, cv, roff, out, tl, lrow, lfirst, cnt, scratch, grp;
+  size_t rp, cv, roff, out, tl, lrow, lfirst, cnt, scratch, grp, usrc, vsrc;
   SplitHost sp;
-  bool has_out;
+  bool has_out, has_usrc, has_vsrc;
 };
 
 SpmmLayout layout_spmm(Arena &ar, const HostCsr &c, int N) {
@@ -165,6 +225,12 @@ SpmmLayout layout_spmm(Arena &ar, const HostCsr &c, int N) {
   L.grp = put(ar, L.sp.groups);
   L.cnt = ar.reserve(L.sp.long_row.size() * sizeof(int32_t));          // zeroed
   L.scratch = ar.reserve(L.sp.task_long.size() * (size_t)N * sizeof(float));
+  L.has_usrc = !L.sp.unit_src.empty();
+  L.usrc = put(ar, L.sp.unit_src);
+  L.has_vsrc = !c.vsrc.empty();
+  if (L.has_vsrc && (int64_t)c.vsrc.size() != c.nnz())
+    throw Error(SHIRO_E_INTERNAL, "refresh map size");
+  L.vsrc = put(ar, c.vsrc);
   return L;
 }
 
@@ -186,7 +252,10 @@ DevSpmm bind_spmm(char *base, const SpmmLayout &L, const HostCsr &c, int N) {
   a.long_first = reinterpret_cast<const int32_t *>(base + L.lfirst);
   a.long_counter = reinterpret_cast<int32_t *>(base + L.cnt);
   a.scratch = reinterpret_cast<float *>(base + L.scratch);
+  a.hot = L.sp.hot ? 1 : 0;
+  a.unit_src = L.has_usrc ? reinterpret_cast<const uint64_t *>(base + L.usrc) : nullptr;
   d.nnz = c.nnz();
+  d.vsrc = L.has_vsrc ? reinterpret_cast<const int32_t *>(base + L.vsrc) : nullptr;
   return d;
 }
 
@@ -211,8 +280,9 @@ void plan_upload(Plan &pl, cudaStream_t s) {
   // second receive buffer for the double-buffered fused exchange
   const bool want2 = pl.P > 1 && !(pl.flags & SHIRO_F_XCHG_NCCL) && dbuf_enabled();
   const size_t o_recv2 = want2 ? ar.reserve((size_t)pl.recv_rows * N * sizeof(float)) : 0;
-  // fused-exchange flags: ready[P], consumed[P], err (IPC-exported with the arena)
-  const size_t o_flags = ar.reserve((2 * (size_t)pl.P + 2) * sizeof(int32_t));
+  // fused-exchange flags: ready[P], consumed[P], err, ep_sig, ep_wait,
+  // done_ctr (IPC-exported with the arena)
+  const size_t o_flags = ar.reserve((2 * (size_t)pl.P + 4) * sizeof(int32_t));
   const bool fused = !(pl.flags & SHIRO_F_SPLIT_RECV);
   SpmmLayout l_diag = layout_spmm(ar, pl.A_diag, N);
   SpmmLayout l_out = layout_spmm(ar, pl.A_out, N);
@@ -250,6 +320,7 @@ void plan_upload(Plan &pl, cudaStream_t s) {
   pl.d_scatter.ptr = reinterpret_cast<const int64_t *>(base + o_sp);
   pl.d_scatter.src = reinterpret_cast<const int32_t *>(base + o_ss);
   pl.d_scatter.nsrc = (int64_t)pl.sc_src.size();
+  pl.refresh_ops = {&pl.d_diag, &pl.d_out, &pl.d_col, &pl.d_rem};
   pl.info.dev_bytes = (int64_t)pl.arena_bytes;
   // per-op algorithmic work (before the host images are dropped)
   auto distinct = [](const std::vector<int32_t> &ids) {
@@ -291,54 +362,57 @@ void plan_drop_host(Plan &pl) {
 }
 
 // Fused producer op of the fused exchange: one SpMM launch whose rows are
-// (1) the packed B rows (one unit-weight nonzero each, K4), (2) the
-// row-based partial rows (A_out, K3) -- both stored at peer addresses -- and
-// (3) the local rows (A_diag, K1) stored into C (tagged row index).  Peer rows
-// come first so their NVLink stores start early.  The hierarchical schedule
-// uses the same launch for Stage I (its pack list holds the B-row unions).
+// (1) the packed B rows (one unit-weight nonzero each, K4) and (2) the
+// row-based partial rows (A_out, K3), both stored at peer addresses; with
+// `with_local` (hierarchical Stage I) also (3) the local rows (A_diag, K1)
+// stored into C (tagged row index).  The flat exchange runs K1 as its own
+// launch concurrently with this one (exec_p2p).
 static bool prod_ops_exist(const Plan &pl) { return pl.prod_ops != nullptr; }
 
 void upload_prod(Plan &pl, const std::vector<int32_t> &pack_src,
                  const std::vector<uint64_t> &pack_addr, const std::vector<uint64_t> &part_addr,
-                 const std::vector<uint64_t> *pack_addr2, const std::vector<uint64_t> *part_addr2) {
+                 bool with_local, const std::vector<uint64_t> *pack_addr2,
+                 const std::vector<uint64_t> *part_addr2) {
   HostCsr c;
   c.ptr_rows = true;
+  c.hot_rows = pl.M;
   std::vector<uint64_t> outp, outp2;
   const bool two = pack_addr2 && part_addr2;
   const int64_t np = (int64_t)pack_src.size();
+  const bool refresh = !pl.A_out.vsrc.empty() || !pl.A_diag.vsrc.empty();
   if (prod_ops_exist(pl)) { cudaFree(pl.prod_ops); pl.prod_ops = nullptr; }
   for (int64_t i = 0; i < np; ++i) {
     c.col.push_back(pack_src[i]);
     c.val.push_back(1.0f);
+    if (refresh) c.vsrc.push_back(-1);
     c.rp.push_back((int64_t)c.col.size());
     outp.push_back(pack_addr[i]);
     if (two) outp2.push_back((*pack_addr2)[i]);
   }
-  for (int64_t t = 0; t < pl.A_out.nrows; ++t) {
-    for (int64_t k = pl.A_out.rp[t]; k < pl.A_out.rp[t + 1]; ++k) {
-      c.col.push_back(pl.A_out.col[k]);
-      c.val.push_back(pl.A_out.val[k]);
+  auto append = [&](const HostCsr &a, int64_t t) {
+    for (int64_t k = a.rp[t]; k < a.rp[t + 1]; ++k) {
+      c.col.push_back(a.col[k]);
+      c.val.push_back(a.val[k]);
+      if (refresh) c.vsrc.push_back(a.vsrc.empty() ? -1 : a.vsrc[k]);
     }
     c.rp.push_back((int64_t)c.col.size());
+  };
+  for (int64_t t = 0; t < pl.A_out.nrows; ++t) {
+    append(pl.A_out, t);
     outp.push_back(part_addr[t]);
     if (two) outp2.push_back((*part_addr2)[t]);
   }
-  for (int64_t t = 0; t < pl.A_diag.nrows; ++t) {
-    for (int64_t k = pl.A_diag.rp[t]; k < pl.A_diag.rp[t + 1]; ++k) {
-      c.col.push_back(pl.A_diag.col[k]);
-      c.val.push_back(pl.A_diag.val[k]);
+  if (with_local)
+    for (int64_t t = 0; t < pl.A_diag.nrows; ++t) {
+      append(pl.A_diag, t);
+      outp.push_back((1ull << 63) | (uint64_t)t);       // local row of C
+      if (two) outp2.push_back((1ull << 63) | (uint64_t)t);
     }
-    c.rp.push_back((int64_t)c.col.size());
-    outp.push_back((1ull << 63) | (uint64_t)t);       // local row of C
-    if (two) outp2.push_back((1ull << 63) | (uint64_t)t);
-  }
   c.nrows = (int64_t)outp.size();
-  c.split_row = np + pl.A_out.nrows;   // peer-destined rows first (early READY)
   Arena ar;
   SpmmLayout L = layout_spmm(ar, c, pl.N);
   const size_t o_ptr = put(ar, outp);
   const size_t o_ptr2 = two ? put(ar, outp2) : 0;
-  const size_t o_sig = ar.reserve(sizeof(int32_t));   // zeroed early-READY counter
   SHIRO_CK(cudaMalloc(&pl.prod_ops, std::max<size_t>(ar.total, 256)));
   SHIRO_CK(cudaMemset(pl.prod_ops, 0, std::max<size_t>(ar.total, 256)));
   char *base = static_cast<char *>(pl.prod_ops);
@@ -349,22 +423,44 @@ void upload_prod(Plan &pl, const std::vector<int32_t> &pack_src,
   pl.d_prod.a.out_ptr = reinterpret_cast<float *const *>(base + o_ptr);
   pl.prod_out_ptr[0] = pl.d_prod.a.out_ptr;
   pl.prod_out_ptr[1] = two ? reinterpret_cast<float *const *>(base + o_ptr2) : nullptr;
-  pl.d_prod.a.sig_rows = c.split_row;
-  pl.d_prod.a.sig_ctr = reinterpret_cast<int32_t *>(base + o_sig);
-  int32_t target = 0;
-  for (const RowGroup &g : L.sp.groups) target += (g.r0 < c.split_row) ? 1 : 0;
-  for (int32_t r : L.sp.long_row) target += (r < c.split_row) ? 1 : 0;
-  pl.d_prod.a.sig_target = target;
+  pl.refresh_ops.push_back(&pl.d_prod);
   pl.info.dev_bytes += (int64_t)ar.total;
-  // the fused launch is the "local" op of a step; pack/partial fold into it
+  // the producer launch carries pack + partial (+ local); its work replaces
+  // those ops in the per-op statistics
   std::vector<int32_t> src(c.col);
   std::sort(src.begin(), src.end());
-  pl.info.op_nnz[SHIRO_OP_LOCAL] = c.nnz();
-  pl.info.op_rows[SHIRO_OP_LOCAL] = c.nrows;
-  pl.info.op_src_rows[SHIRO_OP_LOCAL] = (int64_t)(std::unique(src.begin(), src.end()) - src.begin());
+  const int64_t nsrc = (int64_t)(std::unique(src.begin(), src.end()) - src.begin());
+  const int slot = with_local ? SHIRO_OP_LOCAL : SHIRO_OP_PARTIAL;
+  pl.info.op_nnz[slot] = c.nnz();
+  pl.info.op_rows[slot] = c.nrows;
+  pl.info.op_src_rows[slot] = nsrc;
   pl.info.op_nnz[SHIRO_OP_PACK] = pl.info.op_rows[SHIRO_OP_PACK] = pl.info.op_src_rows[SHIRO_OP_PACK] = 0;
-  pl.info.op_nnz[SHIRO_OP_PARTIAL] = pl.info.op_rows[SHIRO_OP_PARTIAL] = 0;
-  pl.info.op_src_rows[SHIRO_OP_PARTIAL] = 0;
+  if (with_local) {
+    pl.info.op_nnz[SHIRO_OP_PARTIAL] = pl.info.op_rows[SHIRO_OP_PARTIAL] = 0;
+    pl.info.op_src_rows[SHIRO_OP_PARTIAL] = 0;
+  }
+}
+
+// N3 value refresh on the device: upload V, then rewrite the value half of
+// every op's (column, value) pairs through its map.
+void refresh_device(Plan &pl, const std::vector<float> &V, cudaStream_t s) {
+  if (!pl.arena) throw Error(SHIRO_E_ARG, "plan has no device state (SHIRO_F_HOST_ONLY)");
+  const size_t bytes = std::max<size_t>(1, V.size()) * sizeof(float);
+  if (!pl.vspace) SHIRO_CK(cudaMalloc(&pl.vspace, (size_t)std::max<int64_t>(1, pl.nnz_local + pl.nnz_recv_vals) * sizeof(float)));
+  if ((int64_t)V.size() != pl.nnz_local + pl.nnz_recv_vals)
+    throw Error(SHIRO_E_INTERNAL, "refresh: value space size");
+  if (!V.empty()) SHIRO_CK(cudaMemcpyAsync(pl.vspace, V.data(), bytes, cudaMemcpyHostToDevice, s));
+  for (DevSpmm *d : pl.refresh_ops)
+    if (d->vsrc && d->nnz)
+      launch_refresh(d->nnz, d->vsrc, pl.vspace, const_cast<int2 *>(d->a.cv), s);
+  if (pl.route.active) {
+    Route &R = pl.route;
+    for (DevSpmm *d : {&R.d_part, &R.d_agg, &R.d_fin})
+      if (d->vsrc && d->nnz)
+        launch_refresh(d->nnz, d->vsrc, pl.vspace, const_cast<int2 *>(d->a.cv), s);
+  }
+  SHIRO_CK(cudaGetLastError());
+  SHIRO_CK(cudaStreamSynchronize(s));   // V (host) may go away after the call
 }
 
 namespace {
@@ -542,7 +638,7 @@ void hier_resolve(Plan &pl, const std::function<char *(int, int)> &seg,
   // Stage I producers + local rows as one launch (same as the flat fused exchange)
   const size_t n1 = R.s1_pack_dst.size(), n2 = R.s1_part_dst.size();
   upload_prod(pl, R.s1_pack_src, std::vector<uint64_t>(v.begin(), v.begin() + n1),
-              std::vector<uint64_t>(v.begin() + n1, v.begin() + n1 + n2));
+              std::vector<uint64_t>(v.begin() + n1, v.begin() + n1 + n2), true);
 }
 
 // stage 1: B rows and partial C rows -> R1 (peers and self); stage 2: forward
@@ -597,27 +693,30 @@ void exec_hier(Plan &pl, const float *B, float *C, cudaStream_t s) {
 
 // Fused exchange (SHIRO_F_XCHG_NCCL unset, P > 1): K4/K3 store rows straight
 // into the peers' receive buffers over NVLink; flags order the producer and
-// consumer sides (p2p.cu).  One stream, no staging copy, no NCCL kernel.
-//   wait CONSUMED >= e-1 (peers done with my previous rows)
-//   one launch: K4 pack + K3 partial SpMM -> peers' buffers, K1 local -> C
-//   signal READY = e at peers
-//   wait READY >= e from all peers, K2 remote SpMM + K5 scatter-add (fused
-//   by default), signal CONSUMED = e at peers
-// SHIRO_FUSED_STEP=1 runs producer -> READY -> wait -> remote as ONE launch (k_step)
-bool fused_step_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    // opt-in: measured slower than graph-replayed separate launches at P=4
-    // (c4 1.36 vs 1.15 ms, profiles/r1_fused_step_P4.txt)
-    const char *e = getenv("SHIRO_FUSED_STEP");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
-}
-
-// The remote SpMM's warps wait for READY themselves (one launch fewer per
-// step: c2/P=4 0.074 -> 0.068 ms, c4 -0.5 %, profiles/r1_inkernel_wait_P4.txt);
-// SHIRO_INKERNEL_WAIT=0 keeps the separate k_wait launch
+// consumer sides (p2p.cu).  No staging copy, no NCCL kernel.  One step:
+//
+//   s_hi (high priority):  [wait CONSUMED >= e-1, single buffer only]
+//                          producer: K4 pack + K3 partial SpMM -> peers' buffers
+//                          signal READY = e at every peer
+//   s    (caller's stream): K1 local SpMM -> C       (concurrently with s_hi)
+//                          K2+K5 remote SpMM, C += A_rem * recv: each work
+//                          unit waits only for the READY flags of the sources
+//                          its nonzeros read (rows of a peer
+//                          are consumed as soon as they land); the last warp
+//                          also waits for every peer before the step ends
+//                          [signal CONSUMED = e, single buffer only]
+//   join s_hi -> s.
+//
+// Double buffering (default): step e's rows land in the peers' buffer e mod
+// 2.  A peer read that buffer last in its remote SpMM of step e-2, which
+// completed before its step e-1 forked its producer and READY(e-1) -- and
+// this rank's step e-1 ended only after READY(e-1) from every peer.  So no
+// CONSUMED round trip.  The producer runs on a high-priority stream: CTAs of
+// the remote SpMM that spin on a late peer can never keep this GPU's own
+// producer from being scheduled.  Epochs: ep_sig (advanced by the READY
+// signal) and ep_wait (advanced by the remote SpMM's last warp) live in
+// device memory, so the whole step is one replayable CUDA graph.
+// SHIRO_INKERNEL_WAIT=0: the consumer waits for all peers in a k_wait launch.
 bool inkernel_wait_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -627,143 +726,58 @@ bool inkernel_wait_enabled() {
   return v == 1;
 }
 
-// SHIRO_EARLY_READY=1: the producer raises READY from inside its launch once
-// the peer-destined units are stored.  Opt-in: measured slower at P=2 (c4
-// 1.66 vs 1.55 ms, c3 2.81 vs 2.67 ms, profiles/r1_early_ready_P2.txt): the
-// system-scope fence each peer-destined unit needs before it is counted
-// stalls its warp for an NVLink round trip, which costs more than the
-// separate k_signal launch it saves.
-bool early_ready_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char *e = getenv("SHIRO_EARLY_READY");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
-}
-
 void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
   if (*pl.err_host) throw Error(SHIRO_E_PEER, "fused exchange: a peer did not signal in time");
-  auto rec = [&](int i) {
-    if (pl.prof_on) SHIRO_CK(cudaEventRecord(pl.prof[i], s));
+  auto rec = [&](int i, cudaStream_t st) {
+    if (pl.prof_on) SHIRO_CK(cudaEventRecord(pl.prof[i], st));
   };
   const int P = pl.P;
-  int32_t *err = pl.xflags + 2 * P, *ep = pl.xflags + 2 * P + 1;  // device epoch e-1
+  int32_t *err = pl.xflags + 2 * P, *ep_sig = err + 1, *ep_wait = err + 2, *done = err + 3;
   int64_t launches = 0;
-  if (pl.dbuf) {
-    // Double-buffered: step e's rows land in the peers' buffer e mod 2.  A
-    // peer read that buffer last in its remote SpMM of step e-2, which
-    // precedes (stream order) its producer and READY of step e-1, which this
-    // rank waited for before this producer: no CONSUMED wait or signal.
-    //   producer (peer buffer e%2) -> READY = e -> wait READY >= e (sets the
-    //   epoch) -> remote SpMM over my buffer e%2
-    const int par = pl.step_parity;
-    float *rb = par ? pl.recv_buf2 : pl.recv_buf;
-    rec(0); rec(1); rec(2); rec(5);
-    DevSpmm prod = pl.d_prod;
-    prod.a.out_ptr = pl.prod_out_ptr[par];
-    launches += run_spmm(prod, B, pl.M, nullptr, C, false, s);
-    rec(6);
-    int lpr_, vpl_;
-    if (inkernel_wait_enabled() && !(pl.flags & SHIRO_F_SPLIT_RECV) && pl.d_rem.a.nrows > 0 &&
-        !pl.prof_on && vec_shape(pl.N, &lpr_, &vpl_)) {
-      // READY = e with the epoch advanced by the signal kernel; the remote
-      // SpMM's warps wait for READY >= e themselves (3 launches per step)
-      launches += launch_signal(pl.ready_ptrs, P - 1, ep, 1, true, s);
-      rec(3);
-      rec(4);
-      DevSpmm rem = pl.d_rem;
-      rem.a.wait_flags = pl.xflags;
-      rem.a.wait_n = P;
-      rem.a.wait_epoch = ep;
-      rem.a.wait_err = err;
-      rem.a.wait_timeout_ns = pl.wait_timeout_ns;
-      launches += run_spmm(rem, rb, pl.recv_rows, nullptr, C, true, s);
-      rec(7);
-      rec(8);
-      SHIRO_CK(cudaMemcpyAsync(pl.err_host, err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-      pl.last_launches = launches;
-      pl.prof_used = 3;
-      return;
-    }
-    launches += launch_signal(pl.ready_ptrs, P - 1, ep, 1, false, s);
-    rec(3);
-    launches += launch_wait(pl.xflags, P, ep, 1, err, pl.wait_timeout_ns, s, true);
-    rec(4);
-    if (!(pl.flags & SHIRO_F_SPLIT_RECV)) {
+  const int par = pl.dbuf ? pl.step_parity : 0;
+  float *rb = par ? pl.recv_buf2 : pl.recv_buf;
+  // fork: the producer branch
+  rec(0, s);
+  SHIRO_CK(cudaEventRecord(pl.ev_fork, s));
+  SHIRO_CK(cudaStreamWaitEvent(pl.s_hi, pl.ev_fork, 0));
+  if (!pl.dbuf)   // single buffer: every peer consumed my rows of step e-1
+    launches += launch_wait(pl.xflags + P, P, ep_sig, 0, err, pl.wait_timeout_ns, pl.s_hi);
+  DevSpmm prod = pl.d_prod;
+  prod.a.out_ptr = pl.prod_out_ptr[par];
+  launches += run_spmm(prod, B, pl.M, nullptr, C, false, pl.s_hi);
+  rec(1, pl.s_hi);
+  launches += launch_signal(pl.ready_ptrs, P - 1, ep_sig, 1, true, pl.s_hi);
+  rec(2, pl.s_hi);
+  SHIRO_CK(cudaEventRecord(pl.ev_join, pl.s_hi));
+  // consumer branch
+  launches += stage_local(pl, B, C, s);
+  rec(3, s);
+  int lpr_, vpl_;
+  const bool split = pl.flags & SHIRO_F_SPLIT_RECV;
+  if (inkernel_wait_enabled() && !split && pl.d_rem.a.n_groups + pl.d_rem.a.n_tasks > 0 &&
+      vec_shape(pl.N, &lpr_, &vpl_)) {
+    DevSpmm rem = pl.d_rem;
+    rem.a.ready = pl.xflags;
+    rem.a.wait_epoch = ep_wait;
+    rem.a.wait_err = err;
+    rem.a.done_ctr = done;
+    rem.a.wait_all = P;
+    rem.a.wait_timeout_ns = pl.wait_timeout_ns;
+    launches += run_spmm(rem, rb, pl.recv_rows, nullptr, C, true, s);
+  } else {
+    launches += launch_wait(pl.xflags, P, ep_wait, 1, err, pl.wait_timeout_ns, s, true);
+    if (!split) {
       launches += run_spmm(pl.d_rem, rb, pl.recv_rows, nullptr, C, true, s);
-      rec(7);
     } else {
       launches += run_spmm(pl.d_col, rb, pl.recv_rows, nullptr, C, true, s);
-      rec(7);
       launches += launch_scatter_add(pl.d_scatter.nt, pl.d_scatter.tgt, pl.d_scatter.ptr,
                                      pl.d_scatter.src, rb, C, pl.N, s);
     }
-    rec(8);
-    SHIRO_CK(cudaMemcpyAsync(pl.err_host, err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    pl.last_launches = launches;
-    pl.prof_used = 3;
-    return;
   }
-  rec(0);
-  launches += launch_wait(pl.xflags + P, P, ep, 0, err, pl.wait_timeout_ns, s);
-  rec(1);
-  rec(2);
-  rec(5);
-  if (fused_step_enabled() && !(pl.flags & SHIRO_F_SPLIT_RECV) && pl.step_ctr) {
-    // one launch: producer -> READY -> wait -> remote (k_step)
-    StepArgs sa;
-    sa.prod = pl.d_prod.a;
-    sa.prod.X0 = B; sa.prod.n0 = pl.M; sa.prod.X1 = nullptr; sa.prod.Y = C;
-    sa.rem = pl.d_rem.a;
-    sa.rem.X0 = pl.recv_buf; sa.rem.n0 = pl.recv_rows; sa.rem.X1 = nullptr; sa.rem.Y = C;
-    sa.ctr = pl.step_ctr;
-    sa.ready_ptrs = pl.ready_ptrs;
-    sa.n_peers = P - 1;
-    sa.ready_local = pl.xflags;
-    sa.P = P;
-    sa.epoch = ep;
-    sa.err = err;
-    sa.timeout_ns = pl.wait_timeout_ns;
-    SHIRO_CK(cudaMemsetAsync(pl.step_ctr, 0, 4 * sizeof(int), s));
-    const int n = launch_step(sa, s);
-    if (n > 0) {
-      launches += n;
-      rec(6); rec(3); rec(4); rec(7); rec(8);
-      launches += launch_signal(pl.consumed_ptrs, P - 1, ep, 1, true, s);
-      SHIRO_CK(cudaMemcpyAsync(pl.err_host, err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-      pl.last_launches = launches;
-      pl.prof_used = 3;
-      return;
-    }
-  }
-  // producer: peer-destined rows first; the lane group storing the last of
-  // them raises READY at the peers from inside the launch (early READY), so
-  // the exchange drains while the local rows are computed
-  DevSpmm prod = pl.d_prod;
-  const bool early = early_ready_enabled() && prod.a.sig_target > 0 && P > 1;
-  if (early) {
-    prod.a.sig_ptrs = pl.ready_ptrs;
-    prod.a.sig_n = P - 1;
-    prod.a.sig_epoch = ep;
-  }
-  launches += run_spmm(prod, B, pl.M, nullptr, C, false, s);
-  rec(6);
-  if (!early) launches += launch_signal(pl.ready_ptrs, P - 1, ep, 1, false, s);
-  rec(3);
-  launches += launch_wait(pl.xflags, P, ep, 1, err, pl.wait_timeout_ns, s);
-  rec(4);
-  if (!(pl.flags & SHIRO_F_SPLIT_RECV)) {
-    launches += run_spmm(pl.d_rem, pl.recv_buf, pl.recv_rows, nullptr, C, true, s);
-    rec(7);
-  } else {
-    launches += run_spmm(pl.d_col, pl.recv_buf, pl.recv_rows, nullptr, C, true, s);
-    rec(7);
-    launches += launch_scatter_add(pl.d_scatter.nt, pl.d_scatter.tgt, pl.d_scatter.ptr,
-                                   pl.d_scatter.src, pl.recv_buf, C, pl.N, s);
-  }
-  rec(8);
-  launches += launch_signal(pl.consumed_ptrs, P - 1, ep, 1, true, s);
+  rec(4, s);
+  SHIRO_CK(cudaStreamWaitEvent(s, pl.ev_join, 0));
+  if (!pl.dbuf) launches += launch_signal(pl.consumed_ptrs, P - 1, ep_wait, 0, false, s);
+  rec(5, s);
   SHIRO_CK(cudaMemcpyAsync(pl.err_host, err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   pl.last_launches = launches;
   pl.prof_used = 3;
@@ -789,6 +803,10 @@ struct shiro_plan_s {
   std::vector<std::unique_ptr<shiro_plan_s>> views;
   Plan *view = nullptr;                         // borrowed rank view
   int64_t last_launches = 0;
+  // loopback value refresh: planned-matrix value offset of each virtual rank
+  // and (SHIRO_F_TRANSPOSE) the entry permutation A -> A^T
+  std::vector<int64_t> lb_val_off, lb_tperm;
+  int64_t lb_nnz = 0;
   Plan &rank_plan() { return view ? *view : *single; }
 };
 
@@ -995,9 +1013,9 @@ int shiro_get_unique_id(void *id128) {
   });
 }
 
-int shiro_plan(const shiro_dist_t *d, int64_t n, const int64_t *part, const int64_t *row_ptr,
-               const int32_t *col_idx, const float *val, int32_t N, void *stream,
-               shiro_plan_t *out) {
+static int plan_impl(const shiro_dist_t *d, int64_t n, const int64_t *part,
+                     const int64_t *row_ptr, const int32_t *col_idx, const float *val, int32_t N,
+                     const int64_t *w_row, const int64_t *w_col, void *stream, shiro_plan_t *out) {
   if (out) *out = nullptr;
   return guarded([&] {
     auto t0 = std::chrono::steady_clock::now();
@@ -1005,6 +1023,10 @@ int shiro_plan(const shiro_dist_t *d, int64_t n, const int64_t *part, const int6
     const bool host_only = d->flags & SHIRO_F_HOST_ONLY;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     PlanInput in{d->rank, d->nranks, d->group_size, d->flags, n, part, row_ptr, col_idx, val, N};
+    if ((w_row == nullptr) != (w_col == nullptr))
+      throw Error(SHIRO_E_ARG, "w_row and w_col must both be given or both be NULL");
+    in.w_row = w_row;
+    in.w_col = w_col;
     if (d->nranks < 1 || d->rank < 0 || d->rank >= d->nranks)
       throw Error(SHIRO_E_ARG, "bad rank/nranks");
     auto h = std::make_unique<shiro_plan_s>();
@@ -1066,7 +1088,7 @@ int shiro_plan(const shiro_dist_t *d, int64_t n, const int64_t *part, const int6
       xchg(tmsg, trecv);
       trecv.resize(d->nranks);
       trecv[d->rank] = tmsg[d->rank];
-      transpose_assemble(in, trecv, t_rp, t_col, t_val);
+      transpose_assemble(in, trecv, t_rp, t_col, t_val, &pl.tperm);
       in.row_ptr = t_rp.data();
       in.col = t_col.data();
       in.val = t_val.data();
@@ -1101,15 +1123,75 @@ int shiro_plan(const shiro_dist_t *d, int64_t n, const int64_t *part, const int6
       }
       plan_drop_host(pl);
     }
+    // transport of later value refreshes (N3): the caller's host transport
+    // (must outlive the plan) or the plan's NCCL communicator
+    if (d->nranks > 1) {
+      if (d->host_xchg) {
+        shiro_alltoallv_fn fn = d->host_xchg;
+        void *ctx = d->host_xchg_ctx;
+        const int P = d->nranks, r = d->rank;
+        pl.refresh_xchg = [fn, ctx, P, r](const std::vector<std::vector<char>> &snd,
+                                          std::vector<std::vector<char>> &rcv) {
+          callback_alltoallv(fn, ctx, P, r, snd, rcv);
+        };
+      } else if (pl.comm) {
+        ncclComm_t comm = pl.comm;
+        const int P = d->nranks, r = d->rank;
+        cudaStream_t cs = pl.comm_stream;
+        pl.refresh_xchg = [comm, P, r, cs](const std::vector<std::vector<char>> &snd,
+                                           std::vector<std::vector<char>> &rcv) {
+          nccl_host_alltoallv(comm, P, r, cs, snd, rcv);
+        };
+      }
+    }
     pl.info.plan_seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     *out = h.release();
   });
 }
 
-int shiro_plan_loopback(int32_t nranks, int32_t group_size, uint32_t flags, int64_t n,
-                        const int64_t *part, const int64_t *row_ptr, const int32_t *col_idx,
-                        const float *val, int32_t N, void *stream, shiro_plan_t *out) {
+int shiro_plan(const shiro_dist_t *d, int64_t n, const int64_t *part, const int64_t *row_ptr,
+               const int32_t *col_idx, const float *val, int32_t N, void *stream,
+               shiro_plan_t *out) {
+  return plan_impl(d, n, part, row_ptr, col_idx, val, N, nullptr, nullptr, stream, out);
+}
+
+int shiro_plan_weighted(const shiro_dist_t *d, int64_t n, const int64_t *part,
+                        const int64_t *row_ptr, const int32_t *col_idx, const float *val, int32_t N,
+                        const int64_t *w_row, const int64_t *w_col, void *stream,
+                        shiro_plan_t *out) {
+  if (!w_row || !w_col) {
+    if (out) *out = nullptr;
+    return guarded([&] { throw Error(SHIRO_E_ARG, "w_row / w_col is NULL"); });
+  }
+  return plan_impl(d, n, part, row_ptr, col_idx, val, N, w_row, w_col, stream, out);
+}
+
+int shiro_plan_update_values(shiro_plan_t plan, const int64_t *row_ptr, const int32_t *col_idx,
+                             const float *val, void *stream) {
+  return guarded([&] {
+    if (!plan || plan->loopback || plan->view) throw Error(SHIRO_E_ARG, "not a distributed plan");
+    Plan &pl = *plan->single;
+    if (!pl.arena) throw Error(SHIRO_E_ARG, "plan was built with SHIRO_F_HOST_ONLY");
+    if (pl.nnz_local > 0 && !val) throw Error(SHIRO_E_ARG, "val is NULL");
+    if ((pl.flags & SHIRO_F_TRANSPOSE) && (!row_ptr || (pl.M > 0 && !col_idx)))
+      throw Error(SHIRO_E_ARG, "transposed plans need row_ptr and col_idx");
+    if (pl.P > 1 && !pl.refresh_xchg) throw Error(SHIRO_E_ARG, "plan has no refresh transport");
+    auto t0 = std::chrono::steady_clock::now();
+    PlanInput in{pl.rank, pl.P, pl.g, pl.flags, pl.n, pl.part.data(), row_ptr, col_idx, val, pl.N};
+    std::vector<float> V = refresh_value_space(pl, in, val, pl.refresh_xchg);
+    refresh_device(pl, V, static_cast<cudaStream_t>(stream));
+    pl.refresh_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    pl.info.refresh_seconds = pl.refresh_seconds;
+  });
+}
+
+static int plan_loopback_impl(int32_t nranks, int32_t group_size, uint32_t flags, int64_t n,
+                              const int64_t *part, const int64_t *row_ptr,
+                              const int32_t *col_idx, const float *val, int32_t N,
+                              const int64_t *w_row, const int64_t *w_col, void *stream,
+                              shiro_plan_t *out) {
   if (out) *out = nullptr;
   return guarded([&] {
     auto t0 = std::chrono::steady_clock::now();
@@ -1127,6 +1209,10 @@ int shiro_plan_loopback(int32_t nranks, int32_t group_size, uint32_t flags, int6
     std::vector<std::vector<int64_t>> rps(P);
     for (int r = 0; r < P; ++r) {
       PlanInput in{r, P, group_size, flags, n, part, nullptr, nullptr, nullptr, N};
+      if ((w_row == nullptr) != (w_col == nullptr))
+        throw Error(SHIRO_E_ARG, "w_row and w_col must both be given or both be NULL");
+      in.w_row = w_row ? w_row + part[r] : nullptr;
+      in.w_col = w_col;
       if (part[0] != 0 || part[P] != n) throw Error(SHIRO_E_PART, "part[0]/part[P] mismatch");
       if (r == 0 && (flags & SHIRO_F_TRANSPOSE)) {
         // full A^T on the host (validated as A first)
@@ -1135,7 +1221,7 @@ int shiro_plan_loopback(int32_t nranks, int32_t group_size, uint32_t flags, int6
         all.part = part1;
         validate_input(all);
         std::vector<std::vector<char>> one = transpose_messages(all);
-        transpose_assemble(all, one, lb_t_rp, lb_t_col, lb_t_val);
+        transpose_assemble(all, one, lb_t_rp, lb_t_col, lb_t_val, &h->lb_tperm);
         row_ptr = lb_t_rp.data();
         col_idx = lb_t_col.data();
         val = lb_t_val.data();
@@ -1143,6 +1229,9 @@ int shiro_plan_loopback(int32_t nranks, int32_t group_size, uint32_t flags, int6
       for (int p = 0; p < P; ++p)
         if (part[p + 1] < part[p]) throw Error(SHIRO_E_PART, "part must be non-decreasing");
       const int64_t lo = part[r], hi = part[r + 1], base = row_ptr[lo];
+      if (r == 0) { h->lb_val_off.assign(P + 1, 0); h->lb_nnz = row_ptr[n]; }
+      h->lb_val_off[r] = base;
+      h->lb_val_off[r + 1] = row_ptr[hi];
       rps[r].resize(hi - lo + 1);
       for (int64_t t = lo; t <= hi; ++t) rps[r][t - lo] = row_ptr[t] - base;
       in.row_ptr = rps[r].data();
@@ -1233,13 +1322,63 @@ int shiro_plan_loopback(int32_t nranks, int32_t group_size, uint32_t flags, int6
           for (size_t k = 0; k < pl.send_c[d].size(); ++k)
             outp.push_back((uint64_t)(base + (nb + (int64_t)k) * rowb));
         }
-        upload_prod(pl, pl.pack_src, dstp, outp);
+        upload_prod(pl, pl.pack_src, dstp, outp, false);
         pl.p2p = true;      // marks the pointer-routed path (no flags in loopback)
       }
     }
     if (!host_only)
       for (int r = 0; r < P; ++r) plan_drop_host(*h->ranks[r]);
     *out = h.release();
+  });
+}
+
+int shiro_plan_loopback(int32_t nranks, int32_t group_size, uint32_t flags, int64_t n,
+                        const int64_t *part, const int64_t *row_ptr, const int32_t *col_idx,
+                        const float *val, int32_t N, void *stream, shiro_plan_t *out) {
+  return plan_loopback_impl(nranks, group_size, flags, n, part, row_ptr, col_idx, val, N, nullptr,
+                            nullptr, stream, out);
+}
+
+int shiro_plan_loopback_weighted(int32_t nranks, int32_t group_size, uint32_t flags, int64_t n,
+                                 const int64_t *part, const int64_t *row_ptr,
+                                 const int32_t *col_idx, const float *val, int32_t N,
+                                 const int64_t *w_row, const int64_t *w_col, void *stream,
+                                 shiro_plan_t *out) {
+  if (!w_row || !w_col) {
+    if (out) *out = nullptr;
+    return guarded([&] { throw Error(SHIRO_E_ARG, "w_row / w_col is NULL"); });
+  }
+  return plan_loopback_impl(nranks, group_size, flags, n, part, row_ptr, col_idx, val, N, w_row,
+                            w_col, stream, out);
+}
+
+int shiro_plan_update_values_loopback(shiro_plan_t plan, const float *val, void *stream) {
+  return guarded([&] {
+    if (!plan || !plan->loopback || plan->view) throw Error(SHIRO_E_ARG, "not a loopback plan");
+    if (plan->lb_nnz > 0 && !val) throw Error(SHIRO_E_ARG, "val is NULL");
+    const int P = (int)plan->ranks.size();
+    for (auto &p : plan->ranks)
+      if (!p->arena) throw Error(SHIRO_E_ARG, "plan was built with SHIRO_F_HOST_ONLY");
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<float> tv;
+    const float *pv = val;
+    if (!plan->lb_tperm.empty() || (plan->ranks[0]->flags & SHIRO_F_TRANSPOSE)) {
+      tv.resize(plan->lb_nnz);
+      for (int64_t x = 0; x < plan->lb_nnz; ++x) tv[x] = val[plan->lb_tperm[x]];
+      pv = tv.data();
+    }
+    // in-process exchange of the row-based values, then every rank's V
+    std::vector<std::vector<std::vector<char>>> out(P);
+    for (int r = 0; r < P; ++r) out[r] = refresh_ship(*plan->ranks[r], pv + plan->lb_val_off[r]);
+    for (int r = 0; r < P; ++r) {
+      std::vector<std::vector<char>> rcv(P);
+      for (int q = 0; q < P; ++q)
+        if (q != r) rcv[q] = out[q][r];
+      std::vector<float> V = refresh_assemble(*plan->ranks[r], pv + plan->lb_val_off[r], rcv);
+      refresh_device(*plan->ranks[r], V, static_cast<cudaStream_t>(stream));
+    }
+    const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    for (auto &p : plan->ranks) { p->refresh_seconds = sec; p->info.refresh_seconds = sec; }
   });
 }
 
@@ -1294,6 +1433,8 @@ int shiro_spmm_host(shiro_plan_t plan, const float *B_host, float *C_host, void 
     run_step(pl, dB, dC, s);
     if (bytes) SHIRO_CK(cudaMemcpyAsync(C_host, dC, bytes, cudaMemcpyDeviceToHost, s));
     SHIRO_CK(cudaStreamSynchronize(s));
+    if (pl.err_host && *pl.err_host)
+      throw Error(SHIRO_E_PEER, "fused exchange: a peer did not signal in time (C is invalid)");
     plan->last_launches = pl.last_launches;
   });
 }
@@ -1338,6 +1479,8 @@ int shiro_spmm_host_batch(shiro_plan_t plan, int64_t nb, const float *const *B_h
     }
     SHIRO_CK(cudaStreamWaitEvent(s, pl.ev_out, 0));
     SHIRO_CK(cudaStreamSynchronize(s));
+    if (pl.err_host && *pl.err_host)
+      throw Error(SHIRO_E_PEER, "fused exchange: a peer did not signal in time (C is invalid)");
     plan->last_launches = launches;
   });
 }
@@ -1363,12 +1506,16 @@ int shiro_spmm_loopback(shiro_plan_t plan, const float *B, float *C, void *strea
       for (int r = 0; r < P; ++r) launches += hier_stage(*plan->ranks[r], 2, Bp(r), Cp(r), s);
       for (int r = 0; r < P; ++r) launches += hier_stage(*plan->ranks[r], 3, Bp(r), Cp(r), s);
     } else if (plan->ranks[0]->p2p) {
-      // fused producer launches (peer rows + local rows), then the receives
+      // fused producer launches (peer rows), then each rank's local SpMM and
+      // receives
       for (int r = 0; r < P; ++r) {
         Plan &pl = *plan->ranks[r];
         launches += run_spmm(pl.d_prod, Bp(r), pl.M, nullptr, Cp(r), false, s);
       }
-      for (int r = 0; r < P; ++r) launches += stage_recv(*plan->ranks[r], Cp(r), s);
+      for (int r = 0; r < P; ++r) {
+        launches += stage_local(*plan->ranks[r], Bp(r), Cp(r), s);
+        launches += stage_recv(*plan->ranks[r], Cp(r), s);
+      }
     } else {
       for (int r = 0; r < P; ++r) launches += stage_send(*plan->ranks[r], Bp(r), s);
       // exchange: device copies send(s -> r) into recv(r from s)
@@ -1482,14 +1629,17 @@ int shiro_stage_times(shiro_plan_t plan, double *ms) {
       ms[SHIRO_STAGE_TOTAL] = el(0, 6);
       return;
     }
-    if (pl.prof_used == 3) {   // fused exchange: "exchange" = exposed wait for peers
-      ms[SHIRO_STAGE_PACK] = el(0, 1);
-      ms[SHIRO_STAGE_PARTIAL] = el(1, 2);
-      ms[SHIRO_STAGE_LOCAL] = el(5, 6);
-      ms[SHIRO_STAGE_EXCHANGE] = el(3, 4);
-      ms[SHIRO_STAGE_REMOTE] = el(4, 7);
-      ms[SHIRO_STAGE_SCATTER] = el(7, 8);
-      ms[SHIRO_STAGE_TOTAL] = el(0, 8);
+    if (pl.prof_used == 3) {
+      // fused exchange, the same schedule as the timed (graph) step:
+      // PARTIAL = the producer launch (K4 pack + K3 partials -> peers, on the
+      // high-priority branch), EXCHANGE = its READY signal, LOCAL = K1
+      // (concurrent with the producer), REMOTE = the consumer from the end of
+      // K1, including its per-source waits
+      ms[SHIRO_STAGE_PARTIAL] = el(0, 1);
+      ms[SHIRO_STAGE_EXCHANGE] = el(1, 2);
+      ms[SHIRO_STAGE_LOCAL] = el(0, 3);
+      ms[SHIRO_STAGE_REMOTE] = el(3, 4);
+      ms[SHIRO_STAGE_TOTAL] = el(0, 5);
       return;
     }
     ms[SHIRO_STAGE_PACK] = el(0, 1);

@@ -40,15 +40,26 @@ int64_t block_cover(int32_t nr, int32_t nc, const std::vector<int64_t> &ap,
                     std::vector<uint8_t> &sel_col);
 
 
+// weighted canonical block cover (cover.cpp): exact minimum
+// weight cover by max flow on the paper's network
+int64_t block_cover_weighted(int32_t nr, int32_t nc, const std::vector<int64_t> &ap,
+                             const std::vector<int32_t> &adj, const std::vector<int64_t> &w_row,
+                             const std::vector<int64_t> &w_col, bool colmax,
+                             std::vector<uint8_t> &sel_row, std::vector<uint8_t> &sel_col);
+
 // Host CSR of one SpMM op.  out_row empty = identity.
 struct HostCsr {
   int64_t nrows = 0;
   std::vector<int64_t> rp{0};
   std::vector<int32_t> col;
   std::vector<float> val;       // empty = all ones
+  std::vector<int32_t> vsrc;    // per nonzero: index into the plan's value space, -1 = unit
+                                // weight (value refresh, N3); empty = no refresh entries
   std::vector<int32_t> out_row;
   bool ptr_rows = false;        // rows addressed by per-row output pointers
-  int64_t split_row = -1;       // row groups never straddle this row (early READY)
+  std::vector<int64_t> src_bounds;   // non-empty: source s owns columns
+                                     // [src_bounds[s], src_bounds[s+1]) -> per-unit masks
+  int64_t hot_rows = -1;        // >= 0: number of source rows (hot/cold L2 marks)
   int64_t nnz() const { return (int64_t)col.size(); }
 };
 
@@ -56,6 +67,7 @@ struct HostCsr {
 struct DevSpmm {
   SpmmArgs a;            // pointers to device arrays; X/Y filled at run time
   int64_t nnz = 0;
+  const int32_t *vsrc = nullptr;   // refresh map (nnz entries) or nullptr
 };
 
 // Device image of a gather (pack) or gather-sum (scatter) op
@@ -163,7 +175,8 @@ struct Plan {
   // fused NVLink exchange (CUDA IPC peer mappings, p2p_host.cpp)
   bool p2p = false;
   int32_t epoch = 0;
-  int32_t *xflags = nullptr;          // local: ready[P], consumed[P], err
+  // local flags: ready[P], consumed[P], err, ep_sig, ep_wait, done_ctr
+  int32_t *xflags = nullptr;
   int64_t recv_buf_off = 0, flags_off = 0, recv_buf2_off = -1;
   // double buffering: step parity selects the receive buffer peers write
   // (and the producer's destination table); no CONSUMED round trip
@@ -174,11 +187,13 @@ struct Plan {
   void *p2p_arena = nullptr;
   int32_t *const *ready_ptrs = nullptr, *const *consumed_ptrs = nullptr;
   // fused producer launch: pack rows (unit weight) + row-based partials, both
-  // stored into peers' receive buffers, + the local rows into C (K4+K3+K1)
+  // stored into peers' receive buffers (K4+K3); hierarchical Stage I also
+  // carries the local rows into C (K1)
   DevSpmm d_prod;
   void *prod_ops = nullptr;
-  int *step_ctr = nullptr;            // work counters of the fused step kernel
-  int32_t *err_host = nullptr;        // pinned copy of flags[2P]
+  cudaStream_t s_hi = nullptr;        // producer branch of a step (high priority)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int32_t *err_host = nullptr;        // pinned copy of the error flag
   int64_t wait_timeout_ns = 20000000000LL;
   // CUDA graph of one step (P = 1, fused exchange, hierarchical), keyed by
   // (B, C, stream, profiling); replayed while the key matches
@@ -194,6 +209,17 @@ struct Plan {
   float *stage = nullptr;
   cudaStream_t h2d_s = nullptr, d2h_s = nullptr;   // copy engines of the batch pipeline
   cudaEvent_t ev_in = nullptr, ev_comp = nullptr, ev_out = nullptr;
+  // value refresh (N3): value space V = [local values || row-based values
+  // received from each peer, peers ascending]; every device op's nonzeros
+  // map into it (vsrc)
+  int64_t nnz_local = 0, nnz_recv_vals = 0;
+  std::vector<std::vector<int64_t>> ship_idx;   // per q: local nonzeros shipped to q (message order)
+  std::vector<int64_t> recv_vals;               // per peer: row-based values received (count)
+  std::vector<int64_t> tperm;                   // transposed plans: local entry -> received index
+  std::vector<DevSpmm *> refresh_ops;           // device ops carrying values
+  float *vspace = nullptr;                      // device value space (first refresh)
+  Alltoallv refresh_xchg;                       // transport for the refresh exchange
+  double refresh_seconds = 0.0;
 
   ~Plan();
 };
@@ -207,6 +233,8 @@ struct PlanInput {
   const int32_t *col;
   const float *val;
   int32_t N;
+  const int64_t *w_row = nullptr;   // weighted covers (N2): [M_p] cost of this rank's C rows
+  const int64_t *w_col = nullptr;   //   [n] cost of every B row (global ids)
 };
 
 // planner phases (plan.cpp)
@@ -217,6 +245,7 @@ struct Phase1 {
   std::vector<int8_t> tag;                        // per local nonzero: 0 local, 1 row, 2 col
   std::vector<std::vector<int64_t>> recv_b, recv_c;   // what each q sends us
   std::vector<int64_t> n_rows, n_cols, nnz_row;       // per q: |Rows|, |Cols| of A^(p,q)
+  std::vector<std::vector<int64_t>> ship_idx;         // per q: row-based nonzeros, message order
 };
 Phase1 plan_phase1(const PlanInput &in);
 void plan_phase2(const PlanInput &in, Phase1 &p1, const std::vector<std::vector<char>> &in_msgs,
@@ -248,8 +277,10 @@ void p2p_setup(Plan &plan, const Alltoallv &xchg);
 // destination addresses of the packed B rows and of the A_out rows
 void upload_prod(Plan &plan, const std::vector<int32_t> &pack_src,
                  const std::vector<uint64_t> &pack_addr, const std::vector<uint64_t> &part_addr,
-                 const std::vector<uint64_t> *pack_addr2 = nullptr,
+                 bool with_local, const std::vector<uint64_t> *pack_addr2 = nullptr,
                  const std::vector<uint64_t> *part_addr2 = nullptr);
+// value refresh of a plan's device ops from the new value space V (host)
+void refresh_device(Plan &plan, const std::vector<float> &V, cudaStream_t s);
 void plan_drop_host(Plan &plan);
 void p2p_release(Plan &plan);
 void exec_p2p(Plan &plan, const float *B, float *C, cudaStream_t s);
@@ -263,5 +294,14 @@ namespace shiro {
 std::vector<std::vector<char>> transpose_messages(const PlanInput &in);
 void transpose_assemble(const PlanInput &in, const std::vector<std::vector<char>> &msgs,
                         std::vector<int64_t> &rp, std::vector<int32_t> &col,
-                        std::vector<float> &val);
+                        std::vector<float> &val, std::vector<int64_t> *perm = nullptr);
+// value refresh exchange (plan.cpp): new values of this rank's nonzeros ->
+// the plan's value space (transposed plans first redistribute the values)
+std::vector<float> refresh_value_space(Plan &plan, const PlanInput &in, const float *val,
+                                       const Alltoallv &xchg);
+// its two halves (loopback runs the exchange in process): the row-based values
+// this rank ships to each peer, and V from the local values + received ones
+std::vector<std::vector<char>> refresh_ship(const Plan &plan, const float *lv);
+std::vector<float> refresh_assemble(const Plan &plan, const float *lv,
+                                    const std::vector<std::vector<char>> &rcv);
 }  // namespace shiro

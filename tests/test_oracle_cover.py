@@ -172,3 +172,20 @@ def test_konig_on_larger_blocks():
         assert flow == oracle.max_matching_kuhn(nr, nc, list(zip(er.tolist(), ec.tolist())))
         assert np.all(sr[er] | sc[ec])                                  # Eq. 7
         assert sr.sum() + sc.sum() == flow
+
+
+def test_uniform_partition_larger_blocks_first():
+    """S:101 / S:104-106: sizes ceil/floor(n/P), the larger blocks first
+    (10 rows over 4 ranks: 3, 3, 2, 2)."""
+    assert oracle.uniform_partition(10, 4).tolist() == [0, 3, 6, 8, 10]
+    assert oracle.uniform_partition(3, 5).tolist() == [0, 1, 2, 3, 3, 3]   # empty blocks (S:102)
+    assert oracle.uniform_partition(8, 2).tolist() == [0, 4, 8]
+
+
+def test_fig1_setup_bytes():
+    """Fig. 1: the joint cover sends C row 0, whose row-based
+    nonzeros b, c, d (3 entries) are shipped once at plan time:
+    3 x (4 B column + 4 B value) = 24 B (R14)."""
+    plan, _, _ = _block_pair_stats("fig1.txt")
+    assert plan.nnz_row[(1, 0)] == 3
+    assert oracle.volumes(plan, N=1)["setup_bytes"] == 24
