@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Benchmark of the SHIRO distributed SpMM hot path on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--also c4]
+                    [--impl ours|reference]
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
         --master-port P bench.py --gpus N ...
 
@@ -13,7 +14,12 @@ L2 is flushed (a 256 MiB device memset) before every timed step; each step is
 bracketed by synchronize + barrier and timed with CUDA events on the
 launching stream; the per-step time is the max over ranks.
 
-Prints ONE JSON line on rank 0 (see DESIGN.md section 6 for every field).
+The headline workload is c3 (the largest configuration that fits one GPU with
+the most FLOPs); c4 is measured in the same run and reported
+under "also".  Prints ONE JSON line on rank 0 (DESIGN.md section 6 lists every
+field).  Roofline denominators are measured in the same run (FP32 FMA probe,
+float4 HBM copy probe, NVLink peer-store probe at N > 1) next to the
+driver-written MEASURED_PEAKS.json.
 """
 from __future__ import annotations
 
@@ -34,7 +40,6 @@ if ROOT not in sys.path:
 
 METRIC = "SpMM GFLOP/s (2·nnz·N) at 1/2/4/8 B200 + bytes communicated vs oblivious"
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
-NVLINK_GBS = 770.0   # measured peer copy per direction (B200_PROFILING.md); 900 nominal
 
 
 def load_peaks():
@@ -107,7 +112,7 @@ def op_bytes(info, N, op):
         return 12 * r + 4 * z + row * s + 2 * row * r
     b = 8 * z + 8 * (r + 1) + row * s + row * r
     if op != "local":
-        b += 4 * r                       # out_row map
+        b += 4 * r                       # out_row map / per-row output pointer
     if op == "remote":
         b += row * r                     # C read-modify-write
     return b
@@ -115,6 +120,19 @@ def op_bytes(info, N, op):
 
 STAGE_OF_OP = {"local": "local", "partial": "partial", "remote": "remote",
                "scatter": "scatter", "pack": "pack"}
+
+
+def step_terms(info, N):
+    """SURVEY 8(d) per-rank terms of one step: algorithmic HBM bytes, FP32
+    flops and NVLink bytes (max of sent and received rows)."""
+    M = info["m_local"]
+    nnz_g = info["nnz_diag"] + info["nnz_colbased"] + info["nnz_rowbased_computed"]
+    send = info["send_b_rows"] + info["send_c_rows"]
+    recv = info["recv_b_rows"] + info["recv_c_rows"]
+    hbm = 8 * nnz_g + 4 * (M + 1) + 4 * N * M + 4 * N * M + 4 * N * send + 2 * 4 * N * recv
+    flop = 2 * N * nnz_g + N * info["recv_c_rows"]
+    nvl = 4 * N * max(send, recv)
+    return [float(hbm), float(flop), float(nvl), float(nnz_g), float(send), float(recv)]
 
 
 def traffic_from_profiles(config, world, op):
@@ -126,24 +144,55 @@ def traffic_from_profiles(config, world, op):
     return d.get(f"{config}/P{world}/{op}")
 
 
-def gather_probes(sh, torch, dev, stream, Bd, rp_l, col_l, lo, hi, N, flush, reps=5):
+def bytes_table():
+    p = os.path.join(ROOT, "profiles", "bytes_table.json")
+    if not os.path.exists(p):
+        return None
+    return {"source": "host-only plans, scripts/bytes_table.py (profiles/bytes_table.json)",
+            "rows": json.load(open(p))}
+
+
+# ----------------------------------------------------------------- probes
+def timed(fn, stream, torch, reps=5, flush=None):
+    ts = []
+    fn()
+    for _ in range(reps):
+        if flush is not None:
+            flush.zero_()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return float(np.median(ts))
+
+
+def probe_peaks(sh, torch, dev, stream):
+    """FP32 FMA and HBM copy rates of this GPU, measured live."""
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    blocks, iters = sms * 8, 4096
+    out = torch.empty(blocks * 256, device=dev)
+    ms = timed(lambda: sh.probe_fma(out, blocks, iters, stream), stream, torch)
+    fp32 = blocks * 256 * iters * 64 / (ms * 1e-3) / 1e12
+    n = 1 << 28                                   # 1 GiB per buffer
+    x = torch.ones(n, device=dev)
+    y = torch.empty_like(x)
+    ms_c = timed(lambda: sh.probe_copy(x, y, stream), stream, torch)
+    copy = 8 * n / (ms_c * 1e-3) / 1e9
+    del x, y
+    return {"fp32_tflops": round(fp32, 2), "copy_gbs": round(copy, 1), "sms": sms}
+
+
+def gather_probes(sh, torch, dev, stream, Bd, col_l, lo, hi, N, flush, reps=5):
     if N not in (32, 64, 128):
         return None
     res = {}
 
     def timeit(X, idx):
         out = torch.empty(((idx.numel() + 255) // 256, N), device=dev)
-        sh.probe_gather(X, idx, out, 256, stream)
-        ts = []
-        for _ in range(reps):
-            flush.zero_()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            sh.probe_gather(X, idx, out, 256, stream)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            ts.append(e0.elapsed_time(e1))
-        ms = float(np.median(ts))
+        ms = timed(lambda: sh.probe_gather(X, idx, out, 256, stream), stream, torch, reps, flush)
         return ms, idx.numel() * N * 4 / (ms * 1e-3) / 1e9
 
     # the local SpMM's own diagonal-block column stream (CSR order)
@@ -162,6 +211,106 @@ def gather_probes(sh, torch, dev, stream, Bd, rp_l, col_l, lo, hi, N, flush, rep
         res[name] = round(timeit(X, ridx)[1], 1)
         del X
     return res
+
+
+def perm_matrix(n, part, rank, k):
+    """This rank's rows of the NVLink probe matrix: row part[p]+i (i < k) has
+    one nonzero in every other block, column part[q]+i (a perfect matching per
+    block, so every block's canonical cover is its k rows and q ships k rows
+    of N floats to p)."""
+    P = part.size - 1
+    lo, hi = int(part[rank]), int(part[rank + 1])
+    rows = []
+    for t in range(lo, hi):
+        i = t - lo
+        rows.append([int(part[q]) + i for q in range(P) if q != rank and i < k])
+    rp = np.zeros(hi - lo + 1, np.int64)
+    rp[1:] = np.cumsum([len(r) for r in rows])
+    col = np.array([c for r in rows for c in r], np.int32)
+    return rp, col, np.ones(col.size, np.float32)
+
+
+def nvlink_probe(sh, torch, dist, dev, stream, world, rank, nccl_id, N=128, k=1 << 17):
+    """Per-direction NVLink bandwidth of (a) the fused exchange's own peer
+    stores (producer launch of a plan whose every block is a k-row perfect
+    matching: k(P-1) rows of 4N B stored into peers, timed with the plan's
+    stage events) and (b) NCCL all_to_all_single of the same bytes."""
+    n = world * k
+    part = sh.uniform_partition(n, world)
+    rp, col, val = perm_matrix(n, part, rank, k)
+    pl = sh.Plan.distributed(rank, world, n, part, rp, col, val, N, nccl_id=nccl_id,
+                             flags=sh.F_MODE_COL)
+    Bd = torch.ones((k, N), device=dev)
+    Cd = torch.empty((k, N), device=dev)
+    for _ in range(3):
+        pl.spmm(Bd, Cd, stream)
+    torch.cuda.synchronize()
+    pl.profile(True)
+    prod = []
+    for _ in range(10):
+        dist.barrier()
+        pl.spmm(Bd, Cd, stream)
+        torch.cuda.synchronize()
+        prod.append(pl.stage_times()["partial"])
+    pl.profile(False)
+    pl.free()
+    nbytes = (world - 1) * k * N * 4
+    ms = float(np.median(prod))
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ipc = nbytes / (t.item() * 1e-3) / 1e9
+    # NCCL all-to-all of the same per-rank bytes
+    send = torch.ones(world * k * N, device=dev)
+    recv = torch.empty_like(send)
+    for _ in range(3):
+        dist.all_to_all_single(recv, send)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(10):
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dist.all_to_all_single(recv, send)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    t2 = torch.tensor([float(np.median(ts))], dtype=torch.float64, device=dev)
+    dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+    nccl = nbytes / (t2.item() * 1e-3) / 1e9
+    del send, recv
+    return {"ipc_store_gbs": round(ipc, 1), "nccl_alltoall_gbs": round(nccl, 1),
+            "bytes_per_rank": nbytes, "producer_ms": round(t.item(), 5),
+            "how": f"k={k} rows x N={N} fp32 to each of {world - 1} peers per rank; "
+                   "per-direction bytes / max-over-ranks time"}
+
+
+def t_floor(sh, torch, dist, dev, stream, world, rank, nccl_id, N, barrier):
+    """Latency floor of one step: 1 row per non-empty pair and
+    1 nonzero per row at the same P and N."""
+    k = 1
+    n = world * 64
+    part = sh.uniform_partition(n, world)
+    rp, col, val = perm_matrix(n, part, rank, k)
+    pl = sh.Plan.distributed(rank, world, n, part, rp, col, val, N, nccl_id=nccl_id)
+    Bd = torch.ones((64, N), device=dev)
+    Cd = torch.empty((64, N), device=dev)
+    for _ in range(5):
+        pl.spmm(Bd, Cd, stream)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(20):
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        pl.spmm(Bd, Cd, stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    pl.free()
+    t = torch.tensor(ts, dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return round(float(t.median().item()), 5)
 
 
 # ----------------------------------------------------------------- reference arm
@@ -219,8 +368,8 @@ def _cache_dir():
 
 
 def cpu_baseline(cfg, row_ptr, col, val, B_full, target_s=10.0):
-    """The oracle's fp64 product on the host cores (rank 0, N=1 only): the
-    full matrix repeated (or a row sample) for about target_s seconds."""
+    """The oracle's fp64 product on the host cores (rank 0, N=1 only): a row
+    sample of the matrix repeated for about target_s seconds."""
     import oracle
     rows, nnz_s = _sample_rows(row_ptr, budget_nnz=20_000_000)
     t0 = time.perf_counter()
@@ -237,50 +386,14 @@ def cpu_baseline(cfg, row_ptr, col, val, B_full, target_s=10.0):
                       f"fp64 accumulation, OpenMP over rows, {t * reps:.1f} s total"}
 
 
-# ----------------------------------------------------------------- main
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2")
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--group-size", type=int, default=1)
-    ap.add_argument("--split-recv", action="store_true", help="SHIRO_F_SPLIT_RECV (K2 and K5 as two launches)")
-    ap.add_argument("--colmax", action="store_true", help="SHIRO_F_COVER_COLMAX")
-    ap.add_argument("--balance", action="store_true", help="SHIRO_F_COVER_BALANCE (R18)")
-    ap.add_argument("--mode", default="joint", choices=["joint", "col", "row"])
-    ap.add_argument("--xchg", default="p2p", choices=["p2p", "nccl"],
-                    help="fused NVLink exchange (default) or NCCL grouped send/recv")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-e2e", action="store_true")
-    args = ap.parse_args()
-    args.warmup = max(args.warmup, 3)
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-
+# ----------------------------------------------------------------- one config
+def measure(cfg_name, args, ctx, primary):
+    """Plan + timed steps + attribution pass + rooflines of one config."""
     import shiro_gen
-    cfg = shiro_gen.CONFIGS[args.config]
-    if args.impl == "reference":
-        run_reference(args, cfg, world, rank)
-        return
-
-    import torch
-    import torch.distributed as dist
-
-    import paper_2512_20178_b200 as sh
-
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
+    sh, torch, dist = ctx["sh"], ctx["torch"], ctx["dist"]
+    world, rank, dev, stream = ctx["world"], ctx["rank"], ctx["dev"], ctx["stream"]
+    barrier = ctx["barrier"]
+    cfg = shiro_gen.CONFIGS[cfg_name]
     row_ptr, col, val = shiro_gen.gen_matrix_shared(cfg, rank, barrier, cache_dir=_cache_dir())
     nnz = int(row_ptr[-1])
     part = sh.uniform_partition(cfg.n, world)
@@ -299,24 +412,13 @@ def main():
     flags |= {"joint": 0, "col": sh.F_MODE_COL, "row": sh.F_MODE_ROW}[args.mode]
     if args.xchg == "nccl":
         flags |= sh.F_XCHG_NCCL
-    nccl_id = None
-    if world > 1:
-        obj = [sh.get_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
     plan = sh.Plan.distributed(rank, world, cfg.n, part, rp_l, col_l, val_l, cfg.N,
-                               group_size=args.group_size, flags=flags, nccl_id=nccl_id)
+                               group_size=args.group_size, flags=flags, nccl_id=ctx["nccl_id"])
     info = plan.info()
 
     Bd = torch.from_numpy(B_p).to(dev)
     Cd = torch.empty((M, cfg.N), device=dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    # a dedicated (capturable) stream: shiro_spmm replays one CUDA graph per step
-    stream = torch.cuda.Stream(device=dev)
-    torch.cuda.set_stream(stream)
-
-    clocks = ClockSampler(local)
-    clocks.start()
+    flush = ctx["flush"]
     for _ in range(args.warmup):
         plan.spmm(Bd, Cd, stream)
     torch.cuda.synchronize()
@@ -338,8 +440,8 @@ def main():
         step_ms.append(ev[k][0].elapsed_time(ev[k][1]))
         launches += plan.last_launches()
     barrier()
-    # attribution pass: the same K steps with per-stage CUDA events (direct
-    # launches on the same stream) -> which kernel dominates and its duration
+    # attribution pass: the same schedule with per-stage CUDA events (direct
+    # launches on the same streams) -> which kernel dominates and its duration
     plan.profile(True)
     for k in range(args.steps):
         flush.zero_()
@@ -353,7 +455,8 @@ def main():
     # max over ranks, per step and per stage
     t = torch.tensor(step_ms, dtype=torch.float64, device=dev)
     st = torch.tensor([[s[x] for x in sh.STAGES] for s in stages], dtype=torch.float64, device=dev)
-    per_rank = None
+    terms = torch.tensor(step_terms(info, cfg.N), dtype=torch.float64, device=dev)
+    per_rank, all_terms = None, [terms]
     if world > 1:
         mine = st.mean(0)
         allr = [torch.empty_like(mine) for _ in range(world)]
@@ -366,6 +469,8 @@ def main():
         dist.all_gather(allw, wk)
         for d_, w_ in zip(per_rank, allw):
             d_["op_nnz"] = {op: int(x) for op, x in zip(sh.OPS, w_.cpu().numpy().tolist()) if x}
+        all_terms = [torch.empty_like(terms) for _ in range(world)]
+        dist.all_gather(all_terms, terms)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(st, op=dist.ReduceOp.MAX)
     step_ms = t.cpu().numpy()
@@ -373,8 +478,8 @@ def main():
     ms = float(step_ms.mean())
     value = 2.0 * nnz * cfg.N / (ms * 1e-3) / 1e9
 
-    # roofline of the dominant kernel (largest mean stage among kernels)
-    peaks = load_peaks()
+    # ---- roofline of the dominant kernel (largest mean stage among kernels)
+    peaks = ctx["peaks"]
     kern = {op: stage_ms[STAGE_OF_OP[op]] for op in sh.OPS if info["op_rows"][op] > 0}
     dom = max(kern, key=kern.get) if kern else "local"
     dom_ms = max(kern.get(dom, 0.0), 1e-9)
@@ -385,19 +490,58 @@ def main():
     achieved = float(ab_all.item()) / (dom_ms * 1e-3) / 1e9
     roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
             "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
-            "traffic": traffic_from_profiles(args.config, world, dom),
+            "traffic": traffic_from_profiles(cfg_name, world, dom),
             "algorithmic_bytes": int(ab_all.item()), "launch_ms": round(dom_ms, 5),
             "peak_source": peaks["source"],
-            "gather_bytes": int(4 * cfg.N * info["op_nnz"][dom]) if dom != "pack" else None}
+            "gather_bytes": int(4 * cfg.N * info["op_nnz"][dom]) if dom != "pack" else None,
+            "timing": "per-stage CUDA events on the launching stream, mean over the K "
+                      "attribution steps, max over ranks"}
+    fp32 = ctx["probes"]["fp32_tflops"]
+    flops_dom = 2.0 * cfg.N * info["op_nnz"][dom]
+    roof["fp32_frac"] = round(flops_dom / (dom_ms * 1e-3) / 1e12 / fp32, 4)
 
-    # gather-aware roofline: the dominant local op's own column stream through
-    # the pure gather probe, plus uniform-random gathers from an L2-resident
-    # (32 MiB) and an HBM-resident (4 GiB) table
-    gather = gather_probes(sh, torch, dev, stream, Bd, rp_l, col_l, lo, hi, cfg.N, flush) \
-        if world == 1 else None      # at P > 1 the dominant launch also carries peer rows
-    if gather and dom == "local":
-        roof["gather_floor_ms"] = gather["csr_stream_ms"]
-        roof["gather_frac"] = round(gather["csr_stream_ms"] / dom_ms, 4)
+    # gather-aware term: the dominant local op's own column stream through the
+    # pure gather probe, plus uniform-random gathers from L2- and HBM-resident
+    # tables
+    gather = None
+    if world == 1 and primary or (world == 1 and args.gather_all):
+        gather = gather_probes(sh, torch, dev, stream, Bd, col_l, lo, hi, cfg.N, flush)
+        if gather and dom == "local":
+            roof["gather_floor_ms"] = gather["csr_stream_ms"]
+            roof["gather_frac"] = round(gather["csr_stream_ms"] / dom_ms, 4)
+
+    # ---- step-level roofline: T_roof = max over ranks of
+    # max(HBM / BW_HBM, FLOP / FP32, NVLink / BW_NVL)
+    nvl_bw = (ctx["nvlink"] or {}).get("ipc_store_gbs")
+    per = []
+    for tr in all_terms:
+        hbm, flop, nvl, nnz_g, snd, rcv = tr.cpu().numpy().tolist()
+        th = hbm / (peaks["hbm_gbs"] * 1e9)
+        tf = flop / (fp32 * 1e12)
+        tn = nvl / (nvl_bw * 1e9) if nvl_bw and nvl > 0 else 0.0
+        per.append({"hbm_bytes": int(hbm), "flop": int(flop), "nvlink_bytes": int(nvl),
+                    "nnz": int(nnz_g), "t_hbm_ms": th * 1e3, "t_fp32_ms": tf * 1e3,
+                    "t_nvl_ms": tn * 1e3})
+    t_roof = max(max(p["t_hbm_ms"], p["t_fp32_ms"], p["t_nvl_ms"]) for p in per)
+    bound_of = lambda p: max((("hbm", p["t_hbm_ms"]), ("fp32", p["t_fp32_ms"]),
+                              ("nvlink", p["t_nvl_ms"])), key=lambda x: x[1])[0]
+    worst = max(per, key=lambda p: max(p["t_hbm_ms"], p["t_fp32_ms"], p["t_nvl_ms"]))
+    nnz_r = [p["nnz"] for p in per]
+    nvl_r = [p["nvlink_bytes"] for p in per]
+    step_roof = {
+        "t_roof_ms": round(t_roof, 5), "t_iter_ms": round(ms, 5),
+        "frac": round(t_roof / ms, 4), "bound": bound_of(worst),
+        "peaks": {"hbm_gbs": peaks["hbm_gbs"], "fp32_tflops": fp32, "nvlink_gbs": nvl_bw},
+        "per_rank": [{k: (round(v, 5) if isinstance(v, float) else v) for k, v in p.items()}
+                     for p in per],
+        "imbalance_nnz_max_over_mean": round(max(nnz_r) / max(1e-9, np.mean(nnz_r)), 4),
+        "imbalance_nvlink_max_over_mean": (round(max(nvl_r) / np.mean(nvl_r), 4)
+                                           if world > 1 and np.mean(nvl_r) > 0 else None)}
+    if gather:
+        step_roof["t_gather_l2_ms"] = round(worst["nnz"] * 4 * cfg.N / (gather["l2_random_gbs"] * 1e9) * 1e3, 5)
+        step_roof["t_gather_hbm_ms"] = round(worst["nnz"] * 4 * cfg.N / (gather["hbm_random_gbs"] * 1e9) * 1e3, 5)
+    if ctx.get("t_floor_ms") is not None:
+        step_roof["t_floor_ms"] = ctx["t_floor_ms"]
 
     # exchange (NVLink) achieved bandwidth, per rank max(send, recv) bytes
     xbytes = 4 * cfg.N * max(info["send_b_rows"] + info["send_c_rows"],
@@ -410,17 +554,128 @@ def main():
         gbs = xb.item() / (stage_ms["exchange"] * 1e-3) / 1e9
         exch = {"mode": "nccl grouped send/recv", "bytes_max_rank": int(xb.item()),
                 "ms": round(stage_ms["exchange"], 5), "achieved_gbs": round(gbs, 1),
-                "peak_gbs": NVLINK_GBS, "frac": round(gbs / NVLINK_GBS, 4)}
+                "peak_gbs": nvl_bw, "frac": round(gbs / nvl_bw, 4) if nvl_bw else None}
     elif world > 1:
-        # fused exchange: the rows cross NVLink inside K4 (pack) and K3
-        # (partial SpMM); only the final flag wait is exposed
-        prod = stage_ms["pack"] + stage_ms["partial"]
+        # fused exchange: the rows cross NVLink inside the producer launch
+        prod = stage_ms["partial"]
         gbs = xb.item() / (prod * 1e-3) / 1e9 if prod > 0 else None
-        exch = {"mode": "fused p2p stores (CUDA IPC over NVLink)", "bytes_max_rank": int(xb.item()),
-                "exposed_wait_ms": round(stage_ms["exchange"], 5),
-                "producer_kernels_ms": round(prod, 5),
-                "achieved_gbs_over_producers": round(gbs, 1) if gbs else None,
-                "peak_gbs": NVLINK_GBS}
+        exch = {"mode": "fused p2p stores (CUDA IPC over NVLink), producer on a high-priority "
+                        "stream concurrent with the local SpMM",
+                "bytes_max_rank": int(xb.item()),
+                "signal_ms": round(stage_ms["exchange"], 5), "producer_ms": round(prod, 5),
+                "achieved_gbs_over_producer": round(gbs, 1) if gbs else None,
+                "peak_gbs": nvl_bw, "frac": round(gbs / nvl_bw, 4) if gbs and nvl_bw else None}
+
+    res = {
+        "config": cfg, "value": value, "ms": ms, "nnz": nnz, "info": info, "roofline": roof,
+        "roofline_step": step_roof, "gather": gather, "exchange": exch, "launches": launches,
+        "stage_ms": stage_ms, "per_rank": per_rank, "step_ms": step_ms,
+        "bytes": {"joint": info["g_joint_rows"] * 4 * cfg.N,
+                  "oblivious_allgather": info["g_oblivious_rows"] * 4 * cfg.N,
+                  "col_based": info["g_col_rows"] * 4 * cfg.N,
+                  "row_based": info["g_row_rows"] * 4 * cfg.N,
+                  "block": info["g_block_rows"] * 4 * cfg.N,
+                  "joint_vs_oblivious": (info["g_joint_rows"] / info["g_oblivious_rows"])
+                  if info["g_oblivious_rows"] else None,
+                  "setup_bytes": info["g_setup_bytes"]},
+    }
+    if primary:
+        res.update(plan=plan, Bd=Bd, B_p=B_p, M=M, row_ptr=row_ptr, col=col, val=val)
+    else:
+        plan.free()
+    return res
+
+
+def summary(r):
+    cfg = r["config"]
+    return {"workload": f"{cfg.name}: {cfg.desc}", "value": round(r["value"], 3), "unit": "GFLOP/s",
+            "ms_per_step": round(r["ms"], 5), "roofline": r["roofline"],
+            "roofline_step": r["roofline_step"], "exchange": r["exchange"],
+            "stages_ms": {k: round(v, 5) for k, v in r["stage_ms"].items()},
+            "bytes": r["bytes"], "plan_seconds": round(r["info"]["plan_seconds"], 3)}
+
+
+# ----------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--also", default=None,
+                    help="comma list of configs measured after the headline one "
+                         "(default: c4 when the headline is c3; 'none' for none)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--group-size", type=int, default=1)
+    ap.add_argument("--split-recv", action="store_true", help="SHIRO_F_SPLIT_RECV (K2 and K5 as two launches)")
+    ap.add_argument("--colmax", action="store_true", help="SHIRO_F_COVER_COLMAX")
+    ap.add_argument("--balance", action="store_true", help="SHIRO_F_COVER_BALANCE (R18)")
+    ap.add_argument("--mode", default="joint", choices=["joint", "col", "row"])
+    ap.add_argument("--xchg", default="p2p", choices=["p2p", "nccl"],
+                    help="fused NVLink exchange (default) or NCCL grouped send/recv")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-probes", action="store_true", help="skip the NVLink / T_floor probes")
+    ap.add_argument("--gather-all", action="store_true", help="gather probes for --also configs too")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    import shiro_gen
+    cfg = shiro_gen.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg, world, rank)
+        return
+    also = args.also if args.also is not None else ("c4" if args.config == "c3" else "none")
+    also = [] if also in ("", "none") else [c for c in also.split(",") if c != args.config]
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2512_20178_b200 as sh
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    nccl_id = None
+    if world > 1:
+        obj = [sh.get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    # a dedicated (capturable) stream: shiro_spmm replays one CUDA graph per step
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    probes = probe_peaks(sh, torch, dev, stream)
+    pt = torch.tensor([probes["fp32_tflops"], probes["copy_gbs"]], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(pt, op=dist.ReduceOp.MIN)
+    probes["fp32_tflops"], probes["copy_gbs"] = [round(x, 2) for x in pt.cpu().numpy().tolist()]
+    nvl = None
+    if world > 1 and not args.no_probes:
+        nvl = nvlink_probe(sh, torch, dist, dev, stream, world, rank, nccl_id)
+    tfl = None
+    if not args.no_probes:
+        tfl = t_floor(sh, torch, dist, dev, stream, world, rank, nccl_id, cfg.N, barrier)
+    ctx = {"sh": sh, "torch": torch, "dist": dist, "world": world, "rank": rank, "dev": dev,
+           "stream": stream, "barrier": barrier, "nccl_id": nccl_id, "peaks": load_peaks(),
+           "probes": probes, "nvlink": nvl, "t_floor_ms": tfl,
+           "flush": torch.empty(256 << 20, dtype=torch.uint8, device=dev)}
+
+    main_r = measure(args.config, args, ctx, primary=True)
+    plan, Bd, B_p, M = main_r["plan"], main_r["Bd"], main_r["B_p"], main_r["M"]
+    nnz = main_r["nnz"]
 
     # end to end through the public API with host buffers (pinned): every
     # step uploads its B_p and downloads its C_p inside the timed region.
@@ -462,17 +717,27 @@ def main():
                "api": "shiro_spmm_host_batch (pipelined over the K steps)",
                "single_call_ms_per_step": round(te_mean * 1e3, 4),
                "single_call_value": round(2.0 * nnz * cfg.N / te_mean / 1e9, 3)}
+    plan.free()
+    launches = main_r["launches"]
+    row_ptr, col, val = main_r["row_ptr"], main_r["col"], main_r["val"]
+    for k in ("plan", "Bd", "B_p", "row_ptr", "col", "val"):
+        main_r.pop(k, None)
+
+    others = {}
+    for c in also:
+        others[c] = summary(measure(c, args, ctx, primary=False))
 
     clk = clocks.stop()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        B_full = B_p if world == 1 else shiro_gen.gen_B(cfg.seed, 0, cfg.n, cfg.N)
-        cpu = cpu_baseline(cfg, row_ptr, col, val, B_full)
+        cpu = cpu_baseline(cfg, row_ptr, col, val, shiro_gen.gen_B(cfg.seed, 0, cfg.n, cfg.N))
 
     if rank == 0:
+        step_ms = main_r["step_ms"]
         out = {
-            "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 5),
+            "metric": METRIC, "value": round(main_r["value"], 3), "unit": "GFLOP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(main_r["ms"], 5),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": f"{cfg.name}: {cfg.desc}", "n": cfg.n, "nnz": nnz, "N": cfg.N,
@@ -484,30 +749,29 @@ def main():
                        "l2": "flushed (256 MiB memset) before every timed step",
                        "exchange": (args.xchg if world > 1 else "none"),
                        "parallelism": f"1D row partition over {world} rank(s)"},
-            "roofline": roof,
+            "roofline": main_r["roofline"],
+            "roofline_step": main_r["roofline_step"],
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clk,
-            "bytes": {"joint": info["g_joint_rows"] * 4 * cfg.N,
-                      "oblivious_allgather": info["g_oblivious_rows"] * 4 * cfg.N,
-                      "col_based": info["g_col_rows"] * 4 * cfg.N,
-                      "row_based": info["g_row_rows"] * 4 * cfg.N,
-                      "block": info["g_block_rows"] * 4 * cfg.N,
-                      "joint_vs_oblivious": (info["g_joint_rows"] / info["g_oblivious_rows"])
-                      if info["g_oblivious_rows"] else None,
-                      "setup_bytes": info["g_setup_bytes"]},
-            "exchange": exch,
-            "gather_probe": gather,
-            "stages_ms": {k: round(v, 5) for k, v in stage_ms.items()},
-            "stages_ms_per_rank": per_rank,
+            "peaks_measured": {"fp32_tflops": probes["fp32_tflops"], "copy_gbs": probes["copy_gbs"],
+                               "nvlink": nvl, "sms": probes["sms"],
+                               "how": "FP32: 8 FMA chains/thread x 8 CTAs/SM; copy: float4 "
+                                      "1 GiB (read+write bytes); min over ranks"},
+            "bytes": main_r["bytes"],
+            "bytes_table": bytes_table(),
+            "exchange": main_r["exchange"],
+            "gather_probe": main_r["gather"],
+            "stages_ms": {k: round(v, 5) for k, v in main_r["stage_ms"].items()},
+            "stages_ms_per_rank": main_r["per_rank"],
             "step_ms": {"median": round(float(np.median(step_ms)), 5),
                         "p10": round(float(np.percentile(step_ms, 10)), 5),
                         "p90": round(float(np.percentile(step_ms, 90)), 5)},
-            "plan_seconds": round(info["plan_seconds"], 3),
+            "plan_seconds": round(main_r["info"]["plan_seconds"], 3),
+            "also": others,
         }
         print(json.dumps(out), flush=True)
-    plan.free()
     if world > 1:
         dist.destroy_process_group()
 

@@ -319,6 +319,16 @@ int shiro_probe_gather(const float *X, int32_t N, const int32_t *idx, int64_t n_
 int shiro_probe_gather_tma(const float *X, int64_t x_rows, int32_t N, const int32_t *idx,
                            int64_t n_idx, float *out, int32_t chunk, int32_t stages, void *stream);
 
+/* Roofline denominators (measurement only, SURVEY 8(d) microbenchmarks):
+ * shiro_probe_fma: `blocks` x 256 threads, each 8 independent FMA chains x 4
+ *   FMAs x `iters` (2 flops each); out: device float[blocks * 256].
+ *   FLOP = blocks * 256 * iters * 64.
+ * shiro_probe_copy: y[0..n) = x[0..n) with float4 loads/stores (n % 4 == 0,
+ *   16-byte aligned device buffers); bytes moved = 8 * n.
+ * Errors: SHIRO_E_ARG, SHIRO_E_CUDA (launch). */
+int shiro_probe_fma(float *out, int32_t blocks, int32_t iters, void *stream);
+int shiro_probe_copy(const float *x, float *y, int64_t n_floats, void *stream);
+
 /* Number of kernel launches the last shiro_spmm* issued on this plan (all
  * virtual ranks for loopback), NCCL kernels excluded. */
 int64_t shiro_last_launches(shiro_plan_t plan);

@@ -110,6 +110,8 @@ def load():
         "shiro_stage_times": [P, P],
         "shiro_probe_gather": [P, I32, P, I64, P, I32, P],
         "shiro_probe_gather_tma": [P, I64, I32, P, I64, P, I32, I32, P],
+        "shiro_probe_fma": [P, I32, I32, P],
+        "shiro_probe_copy": [P, P, I64, P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -154,6 +156,18 @@ def probe_gather_tma(X, idx, out, chunk=256, stages=4, stream=None):
                                          ctypes.c_void_p(idx.data_ptr()), idx.numel(),
                                          ctypes.c_void_p(out.data_ptr()), chunk, stages,
                                          _stream_ptr(stream)))
+
+
+def probe_fma(out, blocks, iters, stream=None):
+    """shiro_probe_fma (FP32 FMA peak probe); out: CUDA float tensor >= blocks*256."""
+    _check(load().shiro_probe_fma(ctypes.c_void_p(out.data_ptr()), blocks, iters,
+                                  _stream_ptr(stream)))
+
+
+def probe_copy(x, y, stream=None):
+    """shiro_probe_copy (HBM copy probe) between two CUDA float tensors."""
+    _check(load().shiro_probe_copy(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()),
+                                   x.numel(), _stream_ptr(stream)))
 
 
 def get_unique_id() -> bytes:

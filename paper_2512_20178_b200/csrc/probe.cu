@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "../../include/shiro.h"
 
 namespace {
@@ -125,6 +127,33 @@ __global__ void __launch_bounds__(32) k_probe_gather_tma(const __grid_constant__
   reinterpret_cast<float4 *>(out + blockIdx.x * 128LL)[li] = acc;
 }
 
+// ---- roofline denominators (SURVEY 8(d) microbenchmarks) ------------------
+// FP32 FMA: 8 independent dependency chains per thread, 4 FMAs per chain per
+// iteration; every thread stores its sum (no dead code).
+__global__ void __launch_bounds__(256) k_probe_fma(float *__restrict__ out, int iters) {
+  const float m = 0.9999999f, c = 1e-7f;
+  float a[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = (float)(threadIdx.x + j) * 1e-3f;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[j] = fmaf(a[j], m, c);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s += a[j];
+  out[(int64_t)blockIdx.x * 256 + threadIdx.x] = s;
+}
+
+// HBM copy: float4 grid-stride copy (read + write bytes)
+__global__ void __launch_bounds__(256) k_probe_copy(const float4 *__restrict__ x,
+                                                    float4 *__restrict__ y, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256)
+    y[i] = __ldcs(x + i);
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -178,5 +207,24 @@ extern "C" int shiro_probe_gather(const float *X, int32_t N, const int32_t *idx,
   if (lpr == 32) k_probe_gather<32><<<(unsigned)grid, 256, 0, s>>>(X, N, idx, n_idx, chunk, out);
   else if (lpr == 16) k_probe_gather<16><<<(unsigned)grid, 256, 0, s>>>(X, N, idx, n_idx, chunk, out);
   else k_probe_gather<8><<<(unsigned)grid, 256, 0, s>>>(X, N, idx, n_idx, chunk, out);
+  return cudaGetLastError() == cudaSuccess ? SHIRO_OK : SHIRO_E_CUDA;
+}
+
+extern "C" int shiro_probe_fma(float *out, int32_t blocks, int32_t iters, void *stream) {
+  if (!out || blocks < 1 || iters < 1) return SHIRO_E_ARG;
+  k_probe_fma<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(out, iters);
+  return cudaGetLastError() == cudaSuccess ? SHIRO_OK : SHIRO_E_CUDA;
+}
+
+extern "C" int shiro_probe_copy(const float *x, float *y, int64_t n_floats, void *stream) {
+  if (!x || !y || n_floats < 0 || n_floats % 4) return SHIRO_E_ARG;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t n4 = n_floats / 4;
+  if (n4 == 0) return SHIRO_OK;
+  const int64_t grid = std::min<int64_t>((n4 + 255) / 256, (int64_t)sms * 8);
+  k_probe_copy<<<(unsigned)grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const float4 *>(x), reinterpret_cast<float4 *>(y), n4);
   return cudaGetLastError() == cudaSuccess ? SHIRO_OK : SHIRO_E_CUDA;
 }
