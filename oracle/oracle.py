@@ -306,6 +306,40 @@ def plan_flat(n, part, row_ptr, col, mode="joint", rule="rowmax", balance=False,
     return plan
 
 
+def plan_flat_digests(n, part, row_ptr, col):
+    """The joint row-max lists of plan_flat (same steps: P:315-375 cover per
+    block, R1 read-off, R2 assignment), streamed one receiving rank p at a
+    time for matrices too large to plan at once (c5): returns
+    {(q, p): (sha256 of send_b as int64 bytes, sha256 of send_c, |send_b|,
+    |send_c|)} for every non-empty block.  Memory ~ the rows of one rank."""
+    import hashlib
+    part = np.asarray(part, np.int64)
+    P = part.size - 1
+    out = {}
+    for p in range(P):
+        lo, hi = int(part[p]), int(part[p + 1])
+        k0, k1 = int(row_ptr[lo]), int(row_ptr[hi])
+        gi = np.repeat(np.arange(lo, hi, dtype=np.int64), np.diff(row_ptr[lo:hi + 1]))
+        gj = np.asarray(col[k0:k1], np.int64)
+        qo = owner_of(part, gj)
+        order = np.argsort(qo, kind="stable")
+        bounds = np.searchsorted(qo[order], np.arange(P + 1))
+        for q in range(P):
+            if q == p or bounds[q + 1] == bounds[q]:
+                continue
+            idx = order[bounds[q]:bounds[q + 1]]
+            bi, bj = gi[idx], gj[idx]
+            sel_r, sel_c, mu = min_cover(bi, bj)
+            is_row = np.isin(bi, sel_r)
+            send_c = np.unique(bi[is_row]).astype(np.int64)
+            send_b = np.unique(bj[~is_row]).astype(np.int64)
+            assert send_b.size + send_c.size == mu
+            out[(q, p)] = (hashlib.sha256(send_b.tobytes()).hexdigest(),
+                           hashlib.sha256(send_c.tobytes()).hexdigest(), send_b.size, send_c.size)
+        del gi, gj, qo, order
+    return out
+
+
 def volumes(plan: FlatPlan, N: int, sz: int = 4) -> dict:
     """Volume accounting in rows and bytes (rows * N * sz):
     joint = sum mu (Eq. 10), col = sum |Cols| (Eq. 2),
@@ -569,6 +603,6 @@ __all__ = [
     "ROW", "COL", "LOCAL", "build_oracle_lib", "uniform_partition", "owner_of",
     "spmm_ref", "min_cover_local", "min_cover", "brute_force_cover",
     "max_matching_kuhn", "FlatPlan", "balance_slack", "plan_flat", "volumes", "Msg", "rep_col",
-    "rep_row", "plan_hier", "tier_traffic", "flat_inter_rows", "exec_flat",
+    "rep_row", "plan_hier", "tier_traffic", "flat_inter_rows", "exec_flat", "plan_flat_digests",
     "exec_hier",
 ]

@@ -180,3 +180,22 @@ def test_hier_fixture_lists(name):
             if p != r and p // g != r // g:
                 inter += v.list(p, sh.LIST_H1_SEND).size + v.list(p, sh.LIST_H2_SEND).size
     assert inter == 4                                     # 8 -> 4
+
+
+def test_streamed_digests_match_full_plan_and_library():
+    """oracle.plan_flat_digests (the per-rank streamed form used for c5) gives
+    the same lists as plan_flat, and the library's host-only lists hash to the
+    same digests (c2, P = 4)."""
+    import hashlib
+    from test_c5 import lib_digests
+    c = shiro_gen.CONFIGS["c2"]
+    rp, col, val = shiro_gen.gen_matrix("c2")
+    part = oracle.uniform_partition(c.n, 4)
+    dig = oracle.plan_flat_digests(c.n, part, rp, col)
+    op = oracle.plan_flat(c.n, part, rp, col)
+    h = lambda a: hashlib.sha256(np.asarray(a, np.int64).tobytes()).hexdigest()
+    empty = np.empty(0, np.int64)
+    for k, (db, dc, nb, nc) in dig.items():
+        assert db == h(op.send_b.get(k, empty)) and dc == h(op.send_c.get(k, empty))
+    pl = sh.Plan.loopback(4, c.n, part, rp, col, val, c.N, flags=sh.F_HOST_ONLY)
+    assert lib_digests(pl, 4) == dig
