@@ -413,7 +413,7 @@ def measure(cfg_name, args, ctx, primary):
     if args.xchg == "nccl":
         flags |= sh.F_XCHG_NCCL
     plan = sh.Plan.distributed(rank, world, cfg.n, part, rp_l, col_l, val_l, cfg.N,
-                               group_size=args.group_size, flags=flags, nccl_id=ctx["nccl_id"])
+                               group_size=args.group_size, flags=flags, nccl_id=ctx["fresh_id"]())
     info = plan.info()
 
     Bd = torch.from_numpy(B_p).to(dev)
@@ -646,11 +646,13 @@ def main():
         if world > 1:
             dist.barrier()
 
-    nccl_id = None
-    if world > 1:
+    def fresh_id():
+        """A new ncclUniqueId for each plan's communicator (ids are single-use)."""
+        if world == 1:
+            return None
         obj = [sh.get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        return obj[0]
     # a dedicated (capturable) stream: shiro_spmm replays one CUDA graph per step
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
@@ -664,12 +666,12 @@ def main():
     probes["fp32_tflops"], probes["copy_gbs"] = [round(x, 2) for x in pt.cpu().numpy().tolist()]
     nvl = None
     if world > 1 and not args.no_probes:
-        nvl = nvlink_probe(sh, torch, dist, dev, stream, world, rank, nccl_id)
+        nvl = nvlink_probe(sh, torch, dist, dev, stream, world, rank, fresh_id())
     tfl = None
     if not args.no_probes:
-        tfl = t_floor(sh, torch, dist, dev, stream, world, rank, nccl_id, cfg.N, barrier)
+        tfl = t_floor(sh, torch, dist, dev, stream, world, rank, fresh_id(), cfg.N, barrier)
     ctx = {"sh": sh, "torch": torch, "dist": dist, "world": world, "rank": rank, "dev": dev,
-           "stream": stream, "barrier": barrier, "nccl_id": nccl_id, "peaks": load_peaks(),
+           "stream": stream, "barrier": barrier, "fresh_id": fresh_id, "peaks": load_peaks(),
            "probes": probes, "nvlink": nvl, "t_floor_ms": tfl,
            "flush": torch.empty(256 << 20, dtype=torch.uint8, device=dev)}
 

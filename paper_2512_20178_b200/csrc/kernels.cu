@@ -108,6 +108,18 @@ __device__ __forceinline__ void add4(float4 &acc, const float4 &x) {
   acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
 }
 
+// Source row in the unified row space [X0 || X1] (X1 unused when n0 covers all).
+// (one IMAD.WIDE.U32 per row: column ids and N are non-negative 32-bit)
+template <bool TWO>
+__device__ __forceinline__ const float *src_row_ptr(const SpmmArgs &a, int c) {
+  if (TWO && c >= a.n0) return a.X1 + (uint64_t)(uint32_t)(c - (int)a.n0) * (uint32_t)a.N;
+  return a.X0 + (uint64_t)(uint32_t)c * (uint32_t)a.N;
+}
+template <bool TWO>
+__device__ __forceinline__ const float4 *src_row(const SpmmArgs &a, int c) {
+  return reinterpret_cast<const float4 *>(src_row_ptr<TWO>(a, c));
+}
+
 __device__ __forceinline__ uint64_t gtimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -144,6 +156,18 @@ __device__ __noinline__ bool wait_sources(const int32_t *ready, uint64_t need, i
   return true;
 }
 
+// L2 prefetch of the source row of this lane's nonzero (PF): every lane of a
+// batch requests its whole row (N*4 bytes = N/32 lines of 128 B) before the
+// lane group gathers the batch U rows at a time, so up to LPR rows per lane
+// group are in flight at the L2/DRAM level while only U are held in
+// registers.  No registers are tied up by a prefetch.
+template <bool TWO>
+__device__ __forceinline__ void prefetch_row(const SpmmArgs &a, int c) {
+  const char *r = reinterpret_cast<const char *>(src_row_ptr<TWO>(a, c & 0x7fffffff));   // any HINT
+  for (int off = 0; off < a.N * 4; off += 128)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(r + off));
+}
+
 // Output row address of a pointer-routed row: a peer (or own) buffer address,
 // or -- top bit set -- a row index into Y (the caller's C: local rows of the
 // hierarchical Stage-I launch, whose address is only known at call time).
@@ -152,12 +176,6 @@ __device__ __forceinline__ float4 *out_addr(const SpmmArgs &a, long long v) {
   return reinterpret_cast<float4 *>(v);
 }
 
-// Source row in the unified row space [X0 || X1] (X1 unused when n0 covers all).
-template <bool TWO>
-__device__ __forceinline__ const float4 *src_row(const SpmmArgs &a, int c) {
-  if (TWO && c >= a.n0) return reinterpret_cast<const float4 *>(a.X1 + (int64_t)(c - a.n0) * a.N);
-  return reinterpret_cast<const float4 *>(a.X0 + (int64_t)c * a.N);
-}
 
 // Gather U source rows for nonzeros j..j+U-1 of the current batch; the
 // weights are broadcast together with the columns, before any FMA.
@@ -169,9 +187,10 @@ __device__ __forceinline__ void gather(const SpmmArgs &a, float4 (&x)[U][VPL], f
     const int cu = __shfl_sync(mask, c, j + u, LPR);
     const float vu = __shfl_sync(mask, v, j + u, LPR);
     if (j + u < cnt) {               // uniform across the lane group
-      const float4 *r = src_row<TWO>(a, cu & 0x7fffffff);
+      // hot marks (bit 31) exist only in HINT 3 launches
+      const float4 *r = src_row<TWO>(a, HINT == 3 ? (cu & 0x7fffffff) : cu);
 #pragma unroll
-      for (int q = 0; q < VPL; ++q) x[u][q] = ldB<HINT, COH>(r + li + q * LPR, cu < 0);
+      for (int q = 0; q < VPL; ++q) x[u][q] = ldB<HINT, COH>(r + li + q * LPR, HINT == 3 && cu < 0);
       w[u] = vu;
     } else {
 #pragma unroll
@@ -184,7 +203,8 @@ __device__ __forceinline__ void gather(const SpmmArgs &a, float4 (&x)[U][VPL], f
 // One work unit u: a chunk task (u < n_tasks) or a row group.  OUTP: output
 // rows are addressed by a per-row pointer (e.g. a peer's receive buffer over
 // NVLink, the fused exchange) instead of Y + out_row * N.
-template <int LPR, int VPL, bool ACCUM, bool TWO, int U, bool OUTP, int HINT, bool COH>
+template <int LPR, int VPL, bool ACCUM, bool TWO, int U, bool OUTP, int HINT, bool COH,
+          bool PF = false>
 __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, const int li,
                                           const unsigned mask) {
   float4 acc[VPL];
@@ -203,7 +223,10 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
     for (int64_t base = kb; base < ke; base += LPR) {
       const int64_t k = base + li;
       int2 cv = make_int2(0, 0);
-      if (k < ke) cv = ldcv_h<HINT>(a.cv + k);
+      if (k < ke) {
+        cv = ldcv_h<HINT>(a.cv + k);
+        if (PF) prefetch_row<TWO>(a, cv.x);
+      }
       const int cnt = (int)((ke - base) < LPR ? (ke - base) : LPR);
       for (int j = 0; j < cnt; j += U) {
         float4 x[U][VPL];
@@ -307,6 +330,7 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
     if (k < g.k1) {
       cv = ldcv_h<HINT>(a.cv + k);
       ro = ld_stream_u8(a.roff + k);
+      if (PF) prefetch_row<TWO>(a, cv.x);
     }
     const int cnt = (int)((g.k1 - base) < LPR ? (g.k1 - base) : LPR);
     for (int j = 0; j < cnt; j += U) {
@@ -330,7 +354,7 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
 // N <= 128 (VPL = 1): one-warp CTAs (BS = 32), 32 resident per SM; wider
 // rows (VPL > 1) keep 8-warp CTAs without a residency floor (no spills).
 template <int LPR, int VPL, bool ACCUM, bool TWO, int U, bool OUTP, int HINT, bool WAIT,
-          int BS = 32, int MINB = 32>
+          int BS = 32, int MINB = 32, bool PF = false>
 __global__ void __launch_bounds__(BS, MINB) k_spmm(const SpmmArgs a) {
   constexpr int R = 32 / LPR;   // lane groups per warp
   const int lane = threadIdx.x & 31;
@@ -366,7 +390,7 @@ __global__ void __launch_bounds__(BS, MINB) k_spmm(const SpmmArgs a) {
     }
     return;
   }
-  spmm_unit<LPR, VPL, ACCUM, TWO, (U < LPR ? U : LPR), OUTP, HINT, false>(a, u, li, mask);
+  spmm_unit<LPR, VPL, ACCUM, TWO, (U < LPR ? U : LPR), OUTP, HINT, false, PF>(a, u, li, mask);
 }
 
 // Generic width (N not a supported vector width): one warp per CSR row,
@@ -561,7 +585,7 @@ inline int64_t blocks_for(int64_t units, int rows_per_warp) {
   return (units + per_block - 1) / per_block;
 }
 
-template <int LPR, int VPL, int H>
+template <int LPR, int VPL, int H, bool PF = false>
 void spmm_launch(const SpmmArgs &a, bool acc, cudaStream_t s) {
   constexpr int U = VPL == 1 ? 4 : 8;
   constexpr int BS = VPL == 1 ? 32 : 256, MINB = VPL == 1 ? 32 : 1;
@@ -572,13 +596,13 @@ void spmm_launch(const SpmmArgs &a, bool acc, cudaStream_t s) {
   if (a.ready) {     // fused-exchange consumer: per-source waits, coherent source loads
     k_spmm<LPR, VPL, true, false, U, false, 0, true, BS, MINB><<<grid, BS, 0, s>>>(a);
   } else if (a.out_ptr) {   // fused exchange: overwrite rows in peer buffers
-    k_spmm<LPR, VPL, false, false, U, true, H, false, BS, MINB><<<grid, BS, 0, s>>>(a);
+    k_spmm<LPR, VPL, false, false, U, true, H, false, BS, MINB, PF><<<grid, BS, 0, s>>>(a);
   } else if (acc) {
-    if (two) k_spmm<LPR, VPL, true, true, U, false, H, false, BS, MINB><<<grid, BS, 0, s>>>(a);
-    else k_spmm<LPR, VPL, true, false, U, false, H, false, BS, MINB><<<grid, BS, 0, s>>>(a);
+    if (two) k_spmm<LPR, VPL, true, true, U, false, H, false, BS, MINB, PF><<<grid, BS, 0, s>>>(a);
+    else k_spmm<LPR, VPL, true, false, U, false, H, false, BS, MINB, PF><<<grid, BS, 0, s>>>(a);
   } else {
-    if (two) k_spmm<LPR, VPL, false, true, U, false, H, false, BS, MINB><<<grid, BS, 0, s>>>(a);
-    else k_spmm<LPR, VPL, false, false, U, false, H, false, BS, MINB><<<grid, BS, 0, s>>>(a);
+    if (two) k_spmm<LPR, VPL, false, true, U, false, H, false, BS, MINB, PF><<<grid, BS, 0, s>>>(a);
+    else k_spmm<LPR, VPL, false, false, U, false, H, false, BS, MINB, PF><<<grid, BS, 0, s>>>(a);
   }
 }
 
@@ -592,12 +616,27 @@ int l2_hint(const SpmmArgs &a) {
   return (a.X1 == nullptr && a.n0 * (int64_t)a.N * 4 <= (96ll << 20)) ? 2 : 0;
 }
 
+// L2 prefetch of each batch's source rows (SHIRO_PREFETCH: 1 on, 0 off; by
+// default on when the source rows are far larger than L2, where the gather
+// waits on DRAM)
+bool use_prefetch(const SpmmArgs &a) {
+  static const int env = getenv("SHIRO_PREFETCH") ? atoi(getenv("SHIRO_PREFETCH")) : -1;
+  if (env >= 0) return env == 1;
+  return false;
+}
+
 template <int LPR, int VPL>
 void spmm_shape(const SpmmArgs &a, bool acc, cudaStream_t s) {
   if constexpr (VPL == 1 && LPR >= 8) {
     const int h = l2_hint(a);
+    const bool pf = h != 2 && use_prefetch(a);
     if (h == 2) { spmm_launch<LPR, VPL, 2>(a, acc, s); return; }
-    if (h == 3) { spmm_launch<LPR, VPL, 3>(a, acc, s); return; }
+    if (h == 3) {
+      if (pf) spmm_launch<LPR, VPL, 3, true>(a, acc, s);
+      else spmm_launch<LPR, VPL, 3>(a, acc, s);
+      return;
+    }
+    if (pf) { spmm_launch<LPR, VPL, 0, true>(a, acc, s); return; }
   }
   spmm_launch<LPR, VPL, 0>(a, acc, s);
 }

@@ -273,6 +273,12 @@ bool dbuf_enabled() {
 
 void plan_upload(Plan &pl, cudaStream_t s) {
   SHIRO_CK(cudaGetDevice(&pl.device));
+  // measurement knob: L2 set-aside for persisting (evict_last) lines
+  if (const char *e = getenv("SHIRO_PERSIST_MB")) {
+    const size_t mb = (size_t)atoll(e);
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, mb << 20);
+    cudaGetLastError();
+  }
   Arena ar;
   const int N = pl.N;
   const size_t o_send = ar.reserve((size_t)pl.send_rows * N * sizeof(float));
