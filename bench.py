@@ -152,6 +152,32 @@ def bytes_table():
             "rows": json.load(open(p))}
 
 
+# ----------------------------------------------------------------- NVLink counters
+def nvlink_bytes(gpu_index):
+    """(tx, rx) NVLink data bytes of this GPU since boot, summed over links,
+    from NVML's throughput counters (KiB); None where unsupported."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+        tx = rx = 0
+        got = False
+        for link in range(18):
+            try:
+                v = pynvml.nvmlDeviceGetFieldValues(
+                    h, [(pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, link),
+                        (pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, link)])
+            except Exception:
+                break
+            if v[0].nvmlReturn == 0 and v[1].nvmlReturn == 0:
+                tx += v[0].value.ullVal
+                rx += v[1].value.ullVal
+                got = True
+        return (tx * 1024, rx * 1024) if got else None
+    except Exception:
+        return None
+
+
 # ----------------------------------------------------------------- probes
 def timed(fn, stream, torch, reps=5, flush=None):
     ts = []
@@ -428,6 +454,7 @@ def measure(cfg_name, args, ctx, primary):
           for _ in range(args.steps)]
     step_ms, stages = [], []
     launches = 0
+    nvl0 = nvlink_bytes(ctx["local"]) if world > 1 else None
     # timed region: K steps (each a CUDA-graph replay of shiro_spmm)
     for k in range(args.steps):
         flush.zero_()                                   # L2 flush, outside the timed window
@@ -439,6 +466,7 @@ def measure(cfg_name, args, ctx, primary):
         torch.cuda.synchronize()
         step_ms.append(ev[k][0].elapsed_time(ev[k][1]))
         launches += plan.last_launches()
+    nvl1 = nvlink_bytes(ctx["local"]) if world > 1 else None
     barrier()
     # attribution pass: the same schedule with per-stage CUDA events (direct
     # launches on the same streams) -> which kernel dominates and its duration
@@ -561,6 +589,11 @@ def measure(cfg_name, args, ctx, primary):
         gbs = xb.item() / (prod * 1e-3) / 1e9 if prod > 0 else None
         exch = {"mode": "fused p2p stores (CUDA IPC over NVLink), producer on a high-priority "
                         "stream concurrent with the local SpMM",
+                "nvml_nvlink_tx_bytes_per_step": ((nvl1[0] - nvl0[0]) // args.steps)
+                if nvl0 and nvl1 else None,
+                "nvml_nvlink_rx_bytes_per_step": ((nvl1[1] - nvl0[1]) // args.steps)
+                if nvl0 and nvl1 else None,
+                "expected_send_bytes_this_rank": 4 * cfg.N * (info["send_b_rows"] + info["send_c_rows"]),
                 "bytes_max_rank": int(xb.item()),
                 "signal_ms": round(stage_ms["exchange"], 5), "producer_ms": round(prod, 5),
                 "achieved_gbs_over_producer": round(gbs, 1) if gbs else None,
@@ -632,6 +665,8 @@ def main():
     also = args.also if args.also is not None else ("c4" if args.config == "c3" else "none")
     also = [] if also in ("", "none") else [c for c in also.split(",") if c != args.config]
 
+    if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+        os.environ["NCCL_DEBUG"] = "WARN"       # keep stdout to the one JSON line
     import torch
     import torch.distributed as dist
 
@@ -671,6 +706,7 @@ def main():
     if not args.no_probes:
         tfl = t_floor(sh, torch, dist, dev, stream, world, rank, fresh_id(), cfg.N, barrier)
     ctx = {"sh": sh, "torch": torch, "dist": dist, "world": world, "rank": rank, "dev": dev,
+           "local": local,
            "stream": stream, "barrier": barrier, "fresh_id": fresh_id, "peaks": load_peaks(),
            "probes": probes, "nvlink": nvl, "t_floor_ms": tfl,
            "flush": torch.empty(256 << 20, dtype=torch.uint8, device=dev)}
