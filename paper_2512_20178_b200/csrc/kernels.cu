@@ -65,12 +65,12 @@ __device__ __forceinline__ int2 ldcv_h(const int2 *p) {
   return v;
 }
 // gathered source row: HINT 0 plain LDG; 2 evict_last; 3 evict_last for hot
-// rows, evict_first otherwise; COH: ld.global.cg (coherent at L2: rows that
-// peers store during the launch)
+// rows, evict_first otherwise; COH (and coh for this row): ld.global.cg
+// (coherent at L2: rows that peers store during the launch)
 template <int HINT, bool COH>
-__device__ __forceinline__ float4 ldB(const float4 *p, bool hot) {
+__device__ __forceinline__ float4 ldB(const float4 *p, bool hot, bool coh) {
   float4 v;
-  if (COH) {
+  if (COH && coh) {
     asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];"
                  : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                  : "l"(p));
@@ -189,8 +189,12 @@ __device__ __forceinline__ void gather(const SpmmArgs &a, float4 (&x)[U][VPL], f
     if (j + u < cnt) {               // uniform across the lane group
       // hot marks (bit 31) exist only in HINT 3 launches
       const float4 *r = src_row<TWO>(a, HINT == 3 ? (cu & 0x7fffffff) : cu);
+      // with two sources only the second one (the receive buffer) is written
+      // by peers during the launch
+      const bool coh = !TWO || cu >= a.n0;
 #pragma unroll
-      for (int q = 0; q < VPL; ++q) x[u][q] = ldB<HINT, COH>(r + li + q * LPR, HINT == 3 && cu < 0);
+      for (int q = 0; q < VPL; ++q)
+        x[u][q] = ldB<HINT, COH>(r + li + q * LPR, HINT == 3 && cu < 0, coh);
       w[u] = vu;
     } else {
 #pragma unroll
@@ -593,8 +597,8 @@ void spmm_launch(const SpmmArgs &a, bool acc, cudaStream_t s) {
   const int64_t per_cta = (int64_t)(BS / 32) * (32 / LPR);
   const unsigned grid = (unsigned)((units + per_cta - 1) / per_cta);
   const bool two = a.X1 != nullptr;
-  if (a.ready) {     // fused-exchange consumer: per-source waits, coherent source loads
-    k_spmm<LPR, VPL, true, false, U, false, 0, true, BS, MINB><<<grid, BS, 0, s>>>(a);
+  if (a.ready) {     // fused-exchange consumer (RX): per-source waits, coherent receive-buffer loads
+    k_spmm<LPR, VPL, false, true, U, false, 0, true, BS, MINB><<<grid, BS, 0, s>>>(a);
   } else if (a.out_ptr) {   // fused exchange: overwrite rows in peer buffers
     k_spmm<LPR, VPL, false, false, U, true, H, false, BS, MINB, PF><<<grid, BS, 0, s>>>(a);
   } else if (acc) {

@@ -58,7 +58,9 @@ struct SpmmArgs {
   // sets / sees *wait_err and skips the unit instead of hanging the GPU.
   // The last warp to finish first waits for EVERY source 0..wait_all-1 (the
   // step-end barrier of the double-buffered exchange), then advances
-  // *wait_epoch (done_ctr re-armed).  ready == nullptr: off.
+  // *wait_epoch (done_ctr re-armed).  ready == nullptr: off.  With ready the
+  // launch must be an overwrite with two sources [X0 = B_local || X1 =
+  // receive buffer] (the split consumer RX); only X1 rows use coherent loads.
   const int32_t *ready = nullptr;       // [P] local READY flags (one per source)
   const uint64_t *unit_src = nullptr;   // [n_tasks + n_groups] source masks
   int32_t *wait_epoch = nullptr;

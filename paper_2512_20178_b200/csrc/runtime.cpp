@@ -35,6 +35,9 @@ Plan::~Plan() {
     if (arena) cudaFree(arena);
     if (stage) cudaFree(stage);
     if (vspace) cudaFree(vspace);
+    if (merged_ops) cudaFree(merged_ops);
+    if (s_mid) cudaStreamDestroy(s_mid);
+    if (ev_mid) cudaEventDestroy(ev_mid);
     for (cudaEvent_t e : {ev_in, ev_comp, ev_out})
       if (e) cudaEventDestroy(e);
     if (h2d_s) cudaStreamDestroy(h2d_s);
@@ -185,6 +188,7 @@ SplitHost make_split(const HostCsr &c, int N) {
       uint64_t m = 0;
       for (int64_t k = k0; k < k1; ++k) {
         const int64_t x = c.col[k];
+        if (x < b[0]) continue;                     // local source row (B_local)
         const int src = (int)(std::upper_bound(b.begin(), b.end(), x) - b.begin()) - 1;
         if (src < 0 || src >= (int)b.size() - 1) throw Error(SHIRO_E_INTERNAL, "source of column");
         m |= 1ull << src;
@@ -445,6 +449,78 @@ void upload_prod(Plan &pl, const std::vector<int32_t> &pack_src,
     pl.info.op_nnz[SHIRO_OP_PARTIAL] = pl.info.op_rows[SHIRO_OP_PARTIAL] = 0;
     pl.info.op_src_rows[SHIRO_OP_PARTIAL] = 0;
   }
+}
+
+// Split consumer of the fused exchange: LX = the rows of
+// A_diag without remote entries (overwrite), RX = every row with remote
+// entries, computed whole: its diagonal nonzeros (columns in B_local) then
+// its A_rem entries (columns shifted by M into the receive buffer), overwrite.
+// Disjoint output rows, so LX runs while RX waits for its sources.
+void upload_merged(Plan &pl) {
+  const int64_t M = pl.M;
+  const HostCsr &ad = pl.A_diag, &ar = pl.A_rem;
+  std::vector<uint8_t> has_rem(M, 0);
+  for (int32_t t : ar.out_row) has_rem[t] = 1;
+  const bool refresh = !ad.vsrc.empty();
+  HostCsr lx, rx;
+  lx.hot_rows = M;
+  for (int64_t t = 0; t < M; ++t) {
+    if (has_rem[t]) continue;
+    for (int64_t k = ad.rp[t]; k < ad.rp[t + 1]; ++k) {
+      lx.col.push_back(ad.col[k]);
+      lx.val.push_back(ad.val[k]);
+      if (refresh) lx.vsrc.push_back(ad.vsrc[k]);
+    }
+    lx.rp.push_back((int64_t)lx.col.size());
+    lx.out_row.push_back((int32_t)t);
+  }
+  lx.nrows = (int64_t)lx.out_row.size();
+  for (int64_t i = 0; i < ar.nrows; ++i) {
+    const int64_t t = ar.out_row[i];
+    for (int64_t k = ad.rp[t]; k < ad.rp[t + 1]; ++k) {
+      rx.col.push_back(ad.col[k]);
+      rx.val.push_back(ad.val[k]);
+      if (refresh) rx.vsrc.push_back(ad.vsrc[k]);
+    }
+    for (int64_t k = ar.rp[i]; k < ar.rp[i + 1]; ++k) {
+      rx.col.push_back((int32_t)(M + ar.col[k]));
+      rx.val.push_back(ar.val[k]);
+      if (refresh) rx.vsrc.push_back(ar.vsrc.empty() ? -1 : ar.vsrc[k]);
+    }
+    rx.rp.push_back((int64_t)rx.col.size());
+    rx.out_row.push_back((int32_t)t);
+  }
+  rx.nrows = (int64_t)rx.out_row.size();
+  for (int64_t b : pl.recv_off) rx.src_bounds.push_back(M + b);   // per-unit source masks
+  if ((int64_t)rx.col.size() + M > 0x7fffffffLL || M + pl.recv_rows > 0x7fffffffLL)
+    throw Error(SHIRO_E_ARG, "merged consumer: more than 2^31 source rows");
+  Arena ar2;
+  SpmmLayout L1 = layout_spmm(ar2, lx, pl.N);
+  SpmmLayout L2 = layout_spmm(ar2, rx, pl.N);
+  if (pl.merged_ops) cudaFree(pl.merged_ops);
+  SHIRO_CK(cudaMalloc(&pl.merged_ops, std::max<size_t>(ar2.total, 256)));
+  SHIRO_CK(cudaMemset(pl.merged_ops, 0, std::max<size_t>(ar2.total, 256)));
+  char *base = static_cast<char *>(pl.merged_ops);
+  for (const auto &it : ar2.items)
+    if (it.src && it.bytes)
+      SHIRO_CK(cudaMemcpy(base + it.off, it.src, it.bytes, cudaMemcpyHostToDevice));
+  pl.d_lx = bind_spmm(base, L1, lx, pl.N);
+  pl.d_rx = bind_spmm(base, L2, rx, pl.N);
+  pl.refresh_ops.push_back(&pl.d_lx);
+  pl.refresh_ops.push_back(&pl.d_rx);
+  pl.info.dev_bytes += (int64_t)ar2.total;
+  auto distinct = [](const std::vector<int32_t> &ids) {
+    std::vector<int32_t> v(ids);
+    std::sort(v.begin(), v.end());
+    return (int64_t)(std::unique(v.begin(), v.end()) - v.begin());
+  };
+  pl.info.op_nnz[SHIRO_OP_LOCAL] = lx.nnz();
+  pl.info.op_rows[SHIRO_OP_LOCAL] = lx.nrows;
+  pl.info.op_src_rows[SHIRO_OP_LOCAL] = distinct(lx.col);
+  pl.info.op_nnz[SHIRO_OP_REMOTE] = rx.nnz();
+  pl.info.op_rows[SHIRO_OP_REMOTE] = rx.nrows;
+  pl.info.op_src_rows[SHIRO_OP_REMOTE] = distinct(rx.col);
+  pl.merged = true;
 }
 
 // N3 value refresh on the device: upload V, then rewrite the value half of
@@ -732,6 +808,13 @@ bool inkernel_wait_enabled() {
   return v == 1;
 }
 
+// The split consumer is used with the in-kernel waits, the fused K2+K5 and a
+// vector width (the WAIT kernel); otherwise local SpMM -> k_wait -> remote.
+bool merged_enabled(const Plan &pl) {
+  int lpr, vpl;
+  return inkernel_wait_enabled() && !(pl.flags & SHIRO_F_SPLIT_RECV) && vec_shape(pl.N, &lpr, &vpl);
+}
+
 void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
   if (*pl.err_host) throw Error(SHIRO_E_PEER, "fused exchange: a peer did not signal in time");
   auto rec = [&](int i, cudaStream_t st) {
@@ -742,6 +825,46 @@ void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
   int64_t launches = 0;
   const int par = pl.dbuf ? pl.step_parity : 0;
   float *rb = par ? pl.recv_buf2 : pl.recv_buf;
+  if (pl.merged) {
+    // split consumer: producer (s_hi) || LX (s_mid) || RX (s, per-source waits)
+    rec(0, s);
+    SHIRO_CK(cudaEventRecord(pl.ev_fork, s));
+    SHIRO_CK(cudaStreamWaitEvent(pl.s_hi, pl.ev_fork, 0));
+    SHIRO_CK(cudaStreamWaitEvent(pl.s_mid, pl.ev_fork, 0));
+    if (!pl.dbuf)
+      launches += launch_wait(pl.xflags + P, P, ep_sig, 0, err, pl.wait_timeout_ns, pl.s_hi);
+    DevSpmm prod = pl.d_prod;
+    prod.a.out_ptr = pl.prod_out_ptr[par];
+    launches += run_spmm(prod, B, pl.M, nullptr, C, false, pl.s_hi);
+    rec(1, pl.s_hi);
+    launches += launch_signal(pl.ready_ptrs, P - 1, ep_sig, 1, true, pl.s_hi);
+    rec(2, pl.s_hi);
+    SHIRO_CK(cudaEventRecord(pl.ev_join, pl.s_hi));
+    launches += run_spmm(pl.d_lx, B, pl.M, nullptr, C, false, pl.s_mid);
+    rec(3, pl.s_mid);
+    SHIRO_CK(cudaEventRecord(pl.ev_mid, pl.s_mid));
+    if (pl.d_rx.a.n_groups + pl.d_rx.a.n_tasks > 0) {
+      DevSpmm rx = pl.d_rx;
+      rx.a.ready = pl.xflags;
+      rx.a.wait_epoch = ep_wait;
+      rx.a.wait_err = err;
+      rx.a.done_ctr = done;
+      rx.a.wait_all = P;
+      rx.a.wait_timeout_ns = pl.wait_timeout_ns;
+      launches += run_spmm(rx, B, pl.M, rb, C, false, s);
+    } else {   // nothing received: the step-end barrier alone
+      launches += launch_wait(pl.xflags, P, ep_wait, 1, err, pl.wait_timeout_ns, s, true);
+    }
+    rec(4, s);
+    SHIRO_CK(cudaStreamWaitEvent(s, pl.ev_mid, 0));
+    SHIRO_CK(cudaStreamWaitEvent(s, pl.ev_join, 0));
+    if (!pl.dbuf) launches += launch_signal(pl.consumed_ptrs, P - 1, ep_wait, 0, false, s);
+    rec(5, s);
+    SHIRO_CK(cudaMemcpyAsync(pl.err_host, err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    pl.last_launches = launches;
+    pl.prof_used = 5;
+    return;
+  }
   // fork: the producer branch
   rec(0, s);
   SHIRO_CK(cudaEventRecord(pl.ev_fork, s));
@@ -1329,6 +1452,7 @@ static int plan_loopback_impl(int32_t nranks, int32_t group_size, uint32_t flags
             outp.push_back((uint64_t)(base + (nb + (int64_t)k) * rowb));
         }
         upload_prod(pl, pl.pack_src, dstp, outp, false);
+        if (merged_enabled(pl)) upload_merged(pl);
         pl.p2p = true;      // marks the pointer-routed path (no flags in loopback)
       }
     }
@@ -1519,8 +1643,14 @@ int shiro_spmm_loopback(shiro_plan_t plan, const float *B, float *C, void *strea
         launches += run_spmm(pl.d_prod, Bp(r), pl.M, nullptr, Cp(r), false, s);
       }
       for (int r = 0; r < P; ++r) {
-        launches += stage_local(*plan->ranks[r], Bp(r), Cp(r), s);
-        launches += stage_recv(*plan->ranks[r], Cp(r), s);
+        Plan &pl = *plan->ranks[r];
+        if (pl.merged) {   // split consumer: LX, then RX over [B_local || receive buffer]
+          launches += run_spmm(pl.d_lx, Bp(r), pl.M, nullptr, Cp(r), false, s);
+          launches += run_spmm(pl.d_rx, Bp(r), pl.M, pl.recv_buf, Cp(r), false, s);
+        } else {
+          launches += stage_local(pl, Bp(r), Cp(r), s);
+          launches += stage_recv(pl, Cp(r), s);
+        }
       }
     } else {
       for (int r = 0; r < P; ++r) launches += stage_send(*plan->ranks[r], Bp(r), s);
@@ -1633,6 +1763,18 @@ int shiro_stage_times(shiro_plan_t plan, double *ms) {
       ms[SHIRO_STAGE_PARTIAL] = el(3, 4);
       ms[SHIRO_STAGE_REMOTE] = el(5, 6);
       ms[SHIRO_STAGE_TOTAL] = el(0, 6);
+      return;
+    }
+    if (pl.prof_used == 5) {
+      // split consumer (default fused exchange): PARTIAL = producer (K4 + K3
+      // -> peers), EXCHANGE = its READY signal, LOCAL = LX, REMOTE = RX (rows
+      // with remote entries computed whole, including its per-source waits);
+      // all measured from the step's start (the three branches overlap)
+      ms[SHIRO_STAGE_PARTIAL] = el(0, 1);
+      ms[SHIRO_STAGE_EXCHANGE] = el(1, 2);
+      ms[SHIRO_STAGE_LOCAL] = el(0, 3);
+      ms[SHIRO_STAGE_REMOTE] = el(0, 4);
+      ms[SHIRO_STAGE_TOTAL] = el(0, 5);
       return;
     }
     if (pl.prof_used == 3) {

@@ -191,6 +191,15 @@ struct Plan {
   // carries the local rows into C (K1)
   DevSpmm d_prod;
   void *prod_ops = nullptr;
+  // split consumer of the fused exchange (default): rows without remote
+  // entries (K1 only, "LX") and rows with remote entries computed whole from
+  // [B_local || receive buffer] ("RX": K1 + K2 + K5 of those rows, per-source
+  // waits), disjoint output rows -> the two launches run concurrently
+  bool merged = false;
+  DevSpmm d_lx, d_rx;
+  void *merged_ops = nullptr;
+  cudaStream_t s_mid = nullptr;       // LX branch (priority between producer and RX)
+  cudaEvent_t ev_mid = nullptr;
   cudaStream_t s_hi = nullptr;        // producer branch of a step (high priority)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int32_t *err_host = nullptr;        // pinned copy of the error flag
@@ -282,6 +291,9 @@ void upload_prod(Plan &plan, const std::vector<int32_t> &pack_src,
 // value refresh of a plan's device ops from the new value space V (host)
 void refresh_device(Plan &plan, const std::vector<float> &V, cudaStream_t s);
 void plan_drop_host(Plan &plan);
+// build + upload the split consumer (LX, RX) of the fused exchange
+void upload_merged(Plan &plan);
+bool merged_enabled(const Plan &plan);
 void p2p_release(Plan &plan);
 void exec_p2p(Plan &plan, const float *B, float *C, cudaStream_t s);
 bool dbuf_enabled();   // SHIRO_DBUF (default on): double-buffered fused exchange
