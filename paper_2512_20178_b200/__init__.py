@@ -9,5 +9,5 @@ from .binding import (F_COVER_COLMAX, F_COVER_ROWMAX, F_COVER_BALANCE, F_SPLIT_R
                       F_MODE_BLOCK, F_MODE_COL, F_MODE_JOINT, F_MODE_ROW, F_NO_OVERLAP, F_XCHG_NCCL, LIST_RECV_B,
                       LIST_RECV_C, LIST_SEND_B, LIST_SEND_C, LIST_H1_SEND, LIST_H2_SEND,
                       LIST_H1_RECV, LIST_H2_RECV, Plan, ShiroError, get_unique_id, load,
-                      torch_dist_alltoallv, uniform_partition, local_rows, probe_gather, probe_gather_tma, probe_fma, probe_copy,
+                      torch_dist_alltoallv, uniform_partition, local_rows, probe_gather, probe_gather_tma, probe_gather_tma_ws, probe_fma, probe_copy,
                       STAGES, OPS)

@@ -111,6 +111,7 @@ def load():
         "shiro_probe_gather": [P, I32, P, I64, P, I32, P],
         "shiro_probe_gather_tma": [P, I64, I32, P, I64, P, I32, I32, P],
         "shiro_probe_fma": [P, I32, I32, P],
+        "shiro_probe_gather_tma_ws": [P, I64, I32, P, I64, P, I32, I32, P],
         "shiro_probe_copy": [P, P, I64, P],
     }
     for name, args in sig.items():
@@ -156,6 +157,17 @@ def probe_gather_tma(X, idx, out, chunk=256, stages=4, stream=None):
                                          ctypes.c_void_p(idx.data_ptr()), idx.numel(),
                                          ctypes.c_void_p(out.data_ptr()), chunk, stages,
                                          _stream_ptr(stream)))
+
+
+def probe_gather_tma_ws(X, idx, out, stages=24, ctas=None, stream=None):
+    """shiro_probe_gather_tma_ws (warp-specialized TMA gather4 ring)."""
+    if ctas is None:
+        import torch
+        ctas = 4 * torch.cuda.get_device_properties(X.device).multi_processor_count
+    _check(load().shiro_probe_gather_tma_ws(ctypes.c_void_p(X.data_ptr()), X.shape[0], X.shape[1],
+                                            ctypes.c_void_p(idx.data_ptr()), idx.numel(),
+                                            ctypes.c_void_p(out.data_ptr()), stages, ctas,
+                                            _stream_ptr(stream)))
 
 
 def probe_fma(out, blocks, iters, stream=None):

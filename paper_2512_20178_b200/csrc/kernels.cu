@@ -126,33 +126,33 @@ __device__ __forceinline__ uint64_t gtimer() {
   return t;
 }
 
-// Per-source READY wait of one warp (SpmmArgs::ready): bit s of `need` set ->
-// wait until ready[s] >= target.  Lane s polls source s (P <= 64: two
-// rounds).  Gives up at the warp's own timeout or as soon as another warp
-// has raised *err (one timeout in total, however many waves the grid has).
+// Per-source READY wait of one lane group (SpmmArgs::ready): bit s of `need`
+// set -> wait until ready[s] >= target.  Lane li of the group polls sources
+// li, li + lanes, ... (P <= 64).  Gives up at its own timeout or as soon as
+// another warp has raised *err (one timeout in total, however many waves the
+// grid has).
 __device__ __noinline__ bool wait_sources(const int32_t *ready, uint64_t need, int32_t target,
-                                          int32_t *err, int64_t timeout_ns, int lane) {
+                                          int32_t *err, int64_t timeout_ns, int li, int lanes,
+                                          unsigned mask) {
   const uint64_t t0 = gtimer();
   for (;;) {
     bool ok = true;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int s = lane + 32 * h;
+    for (int s = li; s < 64; s += lanes) {
       if ((need >> s) & 1ull) {
         int32_t v;
         asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(ready + s) : "memory");
         ok = ok && v >= target;
       }
     }
-    if (__all_sync(0xffffffffu, ok)) break;
+    if (__all_sync(mask, ok)) break;
     if (*reinterpret_cast<volatile int32_t *>(err)) return false;
     if ((int64_t)(gtimer() - t0) > timeout_ns) {
-      if (lane == 0) atomicExch(err, 1);
+      if (li == 0) atomicExch(err, 1);
       return false;
     }
     __nanosleep(128);
   }
-  __syncwarp();   // order every lane's source loads after the acquiring lanes
+  __syncwarp(mask);   // order every lane's source loads after the acquiring lanes
   return true;
 }
 
@@ -207,10 +207,21 @@ __device__ __forceinline__ void gather(const SpmmArgs &a, float4 (&x)[U][VPL], f
 // One work unit u: a chunk task (u < n_tasks) or a row group.  OUTP: output
 // rows are addressed by a per-row pointer (e.g. a peer's receive buffer over
 // NVLink, the fused exchange) instead of Y + out_row * N.
+// Unit wait of a two-phase consumer: the sources of unit u's remote part
+// (false: a wait failed -> skip the remote part; the error word is set).
+template <bool WAIT>
+__device__ __forceinline__ bool unit_wait(const SpmmArgs &a, int64_t u, int32_t target, int li,
+                                          int lanes, unsigned mask) {
+  if (!WAIT) return true;
+  const uint64_t need = a.unit_src[u];
+  if (!need) return true;
+  return wait_sources(a.ready, need, target, a.wait_err, a.wait_timeout_ns, li, lanes, mask);
+}
+
 template <int LPR, int VPL, bool ACCUM, bool TWO, int U, bool OUTP, int HINT, bool COH,
-          bool PF = false>
+          bool PF = false, bool PH = false, bool WAIT = false>
 __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, const int li,
-                                          const unsigned mask) {
+                                          const unsigned mask, const int32_t target = 0) {
   float4 acc[VPL];
 #pragma unroll
   for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -224,24 +235,30 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
     const int64_t clen = (re - rb + nch - 1) / nch;     // chunk length of this hub row
     const int64_t kb = rb + (int64_t)(u - f) * clen;
     const int64_t ke = (kb + clen < re) ? kb + clen : re;
-    for (int64_t base = kb; base < ke; base += LPR) {
-      const int64_t k = base + li;
-      int2 cv = make_int2(0, 0);
-      if (k < ke) {
-        cv = ldcv_h<HINT>(a.cv + k);
-        if (PF) prefetch_row<TWO>(a, cv.x);
-      }
-      const int cnt = (int)((ke - base) < LPR ? (ke - base) : LPR);
-      for (int j = 0; j < cnt; j += U) {
-        float4 x[U][VPL];
-        float w[U];
-        gather<LPR, VPL, TWO, U, HINT, COH>(a, x, w, cv.x, __int_as_float(cv.y), j, cnt, li, mask);
+    // two-phase: [kb, kmid) local part, then wait, then [kmid, ke) remote part
+    const int64_t kmid = PH ? (a.long_mid[lr] < kb ? kb : (a.long_mid[lr] > ke ? ke : a.long_mid[lr])) : ke;
+    auto walk = [&](int64_t k0, int64_t k1) {
+      for (int64_t base = k0; base < k1; base += LPR) {
+        const int64_t k = base + li;
+        int2 cv = make_int2(0, 0);
+        if (k < k1) {
+          cv = ldcv_h<HINT>(a.cv + k);
+          if (PF) prefetch_row<TWO>(a, cv.x);
+        }
+        const int cnt = (int)((k1 - base) < LPR ? (k1 - base) : LPR);
+        for (int j = 0; j < cnt; j += U) {
+          float4 x[U][VPL];
+          float w[U];
+          gather<LPR, VPL, TWO, U, HINT, COH>(a, x, w, cv.x, __int_as_float(cv.y), j, cnt, li, mask);
 #pragma unroll
-        for (int uu = 0; uu < U; ++uu)
+          for (int uu = 0; uu < U; ++uu)
 #pragma unroll
-          for (int q = 0; q < VPL; ++q) fma4(acc[q], w[uu], x[uu][q]);
+            for (int q = 0; q < VPL; ++q) fma4(acc[q], w[uu], x[uu][q]);
+        }
       }
-    }
+    };
+    walk(kb, kmid);
+    if (PH && kmid < ke && unit_wait<WAIT>(a, u, target, li, LPR, mask)) walk(kmid, ke);
     float4 *sp = reinterpret_cast<float4 *>(a.scratch + u * (int64_t)a.N);
 #pragma unroll
     for (int q = 0; q < VPL; ++q) __stcg(sp + li + q * LPR, acc[q]);
@@ -291,6 +308,7 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
   const int64_t gi = u - a.n_tasks;
   if (gi >= a.n_groups) return;
   const RowGroup g = a.groups[gi];
+  const int64_t kend = PH ? g.kmid : g.k1;      // phase A (or the whole group)
   const int nrows = g.r1 - g.r0;
   // output rows of the group, one per lane (groups with an out_row map have
   // <= 2*LPR rows, checked at plan time)
@@ -327,16 +345,16 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
     }
     ++cur;
   };
-  for (int64_t base = g.k0; base < g.k1; base += LPR) {
+  for (int64_t base = g.k0; base < kend; base += LPR) {
     const int64_t k = base + li;
     int2 cv = make_int2(0, 0);
     int ro = 0;
-    if (k < g.k1) {
+    if (k < kend) {
       cv = ldcv_h<HINT>(a.cv + k);
       ro = ld_stream_u8(a.roff + k);
       if (PF) prefetch_row<TWO>(a, cv.x);
     }
-    const int cnt = (int)((g.k1 - base) < LPR ? (g.k1 - base) : LPR);
+    const int cnt = (int)((kend - base) < LPR ? (kend - base) : LPR);
     for (int j = 0; j < cnt; j += U) {
       float4 x[U][VPL];
       float w[U];
@@ -353,12 +371,62 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
     }
   }
   while (cur < nrows) flush();              // last row and trailing empty rows
+  if (!PH || g.kmid >= g.k1) return;
+  // ---- phase B (two-phase consumer): the group's remote parts ------------
+  // after its sources' READY; only rows with remote nonzeros are updated
+  // (read-modify-write of rows this unit itself just wrote, in L2)
+  if (!unit_wait<WAIT>(a, u, target, li, LPR, mask)) return;
+  int rcur = -1;
+  auto flush_b = [&]() {
+    int64_t orow;
+    if (a.out_row) {
+      const int sel = (rcur < LPR) ? orw0 : orw1;
+      orow = __shfl_sync(mask, sel, rcur & (LPR - 1), LPR);
+    } else {
+      orow = g.r0 + rcur;
+    }
+    float4 *y = reinterpret_cast<float4 *>(a.Y + orow * a.N);
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) {
+      add4(acc[q], __ldcg(y + li + q * LPR));
+      y[li + q * LPR] = acc[q];
+      acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  for (int64_t base = g.kmid; base < g.k1; base += LPR) {
+    const int64_t k = base + li;
+    int2 cv = make_int2(0, 0);
+    int ro = 0;
+    if (k < g.k1) {
+      cv = ldcv_h<HINT>(a.cv + k);
+      ro = ld_stream_u8(a.roff + k);
+    }
+    const int cnt = (int)((g.k1 - base) < LPR ? (g.k1 - base) : LPR);
+    for (int j = 0; j < cnt; j += U) {
+      float4 x[U][VPL];
+      float w[U];
+      gather<LPR, VPL, TWO, U, HINT, COH>(a, x, w, cv.x, __int_as_float(cv.y), j, cnt, li, mask);
+#pragma unroll
+      for (int uu = 0; uu < U; ++uu) {
+        const int rou = __shfl_sync(mask, ro, j + uu, LPR);
+        if (j + uu < cnt) {
+          if (rou != rcur) {
+            if (rcur >= 0) flush_b();
+            rcur = rou;
+          }
+#pragma unroll
+          for (int q = 0; q < VPL; ++q) fma4(acc[q], w[uu], x[uu][q]);
+        }
+      }
+    }
+  }
+  if (rcur >= 0) flush_b();
 }
 
 // N <= 128 (VPL = 1): one-warp CTAs (BS = 32), 32 resident per SM; wider
 // rows (VPL > 1) keep 8-warp CTAs without a residency floor (no spills).
 template <int LPR, int VPL, bool ACCUM, bool TWO, int U, bool OUTP, int HINT, bool WAIT,
-          int BS = 32, int MINB = 32, bool PF = false>
+          int BS = 32, int MINB = 32, bool PF = false, bool PH = false>
 __global__ void __launch_bounds__(BS, MINB) k_spmm(const SpmmArgs a) {
   constexpr int R = 32 / LPR;   // lane groups per warp
   const int lane = threadIdx.x & 31;
@@ -370,12 +438,8 @@ __global__ void __launch_bounds__(BS, MINB) k_spmm(const SpmmArgs a) {
     // target epoch read before this warp is counted done (the last warp
     // advances it, after every warp has read it)
     const int32_t target = *reinterpret_cast<volatile int32_t *>(a.wait_epoch) + 1;
-    const int64_t units = (int64_t)a.n_tasks + a.n_groups;
-    uint64_t need = (u < units && li == 0) ? a.unit_src[u] : 0ull;
-    // union over the warp's lane groups
-    for (int o = 16; o > 0; o >>= 1) need |= __shfl_xor_sync(0xffffffffu, need, o);
-    const bool ok = wait_sources(a.ready, need, target, a.wait_err, a.wait_timeout_ns, lane);
-    if (ok) spmm_unit<LPR, VPL, ACCUM, TWO, (U < LPR ? U : LPR), OUTP, HINT, true>(a, u, li, mask);
+    spmm_unit<LPR, VPL, ACCUM, TWO, (U < LPR ? U : LPR), OUTP, HINT, true, false, true, true>(
+        a, u, li, mask, target);
     __syncwarp();
     int last = 0;
     if (lane == 0) {
@@ -385,7 +449,7 @@ __global__ void __launch_bounds__(BS, MINB) k_spmm(const SpmmArgs a) {
     if (__shfl_sync(0xffffffffu, last, 0)) {
       // step-end barrier: READY from every peer, also those this rank reads nothing from
       const uint64_t all = a.wait_all >= 64 ? ~0ull : ((1ull << a.wait_all) - 1ull);
-      wait_sources(a.ready, all, target, a.wait_err, a.wait_timeout_ns, lane);
+      wait_sources(a.ready, all, target, a.wait_err, a.wait_timeout_ns, lane, 32, 0xffffffffu);
       if (lane == 0) {
         *a.done_ctr = 0;
         __threadfence();
@@ -394,7 +458,9 @@ __global__ void __launch_bounds__(BS, MINB) k_spmm(const SpmmArgs a) {
     }
     return;
   }
-  spmm_unit<LPR, VPL, ACCUM, TWO, (U < LPR ? U : LPR), OUTP, HINT, false, PF>(a, u, li, mask);
+  // two-phase without waits (loopback): coherent loads of the second source
+  spmm_unit<LPR, VPL, ACCUM, TWO, (U < LPR ? U : LPR), OUTP, HINT, PH, PF, PH, false>(a, u, li,
+                                                                                      mask);
 }
 
 // Generic width (N not a supported vector width): one warp per CSR row,
@@ -597,8 +663,10 @@ void spmm_launch(const SpmmArgs &a, bool acc, cudaStream_t s) {
   const int64_t per_cta = (int64_t)(BS / 32) * (32 / LPR);
   const unsigned grid = (unsigned)((units + per_cta - 1) / per_cta);
   const bool two = a.X1 != nullptr;
-  if (a.ready) {     // fused-exchange consumer (RX): per-source waits, coherent receive-buffer loads
-    k_spmm<LPR, VPL, false, true, U, false, 0, true, BS, MINB><<<grid, BS, 0, s>>>(a);
+  if (a.ready) {     // fused-exchange consumer (CX): per-source waits, coherent receive-buffer loads
+    k_spmm<LPR, VPL, false, true, U, false, 0, true, BS, MINB, false, true><<<grid, BS, 0, s>>>(a);
+  } else if (a.long_mid) {   // two-phase consumer without waits (loopback)
+    k_spmm<LPR, VPL, false, true, U, false, 0, false, BS, MINB, false, true><<<grid, BS, 0, s>>>(a);
   } else if (a.out_ptr) {   // fused exchange: overwrite rows in peer buffers
     k_spmm<LPR, VPL, false, false, U, true, H, false, BS, MINB, PF><<<grid, BS, 0, s>>>(a);
   } else if (acc) {

@@ -16,8 +16,12 @@ namespace shiro {
 // streams a whole group, so the gathers of consecutive short rows are in
 // flight together.
 // A row group: consecutive short rows [r0, r1) whose nonzeros are [k0, k1).
+// Two-phase ops (the fused-exchange consumer) store the group's phase-A
+// nonzeros (every row's local part, row order) in [k0, kmid) and its phase-B
+// nonzeros (every row's remote part, row order) in [kmid, k1); kmid = k1
+// otherwise.
 struct RowGroup {
-  int64_t k0, k1;
+  int64_t k0, k1, kmid;
   int32_t r0, r1;
 };
 
@@ -48,6 +52,12 @@ struct SpmmArgs {
   int32_t *long_counter = nullptr;      // [n_long] zero-initialised arrival counters
   float *scratch = nullptr;             // [n_tasks * N] chunk partials
   int32_t hot = 0;                      // 1: cv carries kHotBit marks (hot/cold L2 policy)
+  // Two-phase op (fused-exchange consumer CX): each row's nonzeros are its
+  // local part (columns < n0, source X0 = B_local) then its remote part
+  // (columns >= n0, X1 = receive buffer); long_mid[l] = first remote nonzero
+  // of long row l.  A unit computes its local parts, then waits for the
+  // sources of its remote parts (when `ready` is set), then adds them.
+  const int64_t *long_mid = nullptr;
   // Per-source wait (fused exchange consumer): unit u reads
   // receive-buffer rows of the sources in unit_src[u] (bit s = source rank
   // s); before it, its warp spins until ready[s] >= *wait_epoch + 1 for
@@ -59,8 +69,8 @@ struct SpmmArgs {
   // The last warp to finish first waits for EVERY source 0..wait_all-1 (the
   // step-end barrier of the double-buffered exchange), then advances
   // *wait_epoch (done_ctr re-armed).  ready == nullptr: off.  With ready the
-  // launch must be an overwrite with two sources [X0 = B_local || X1 =
-  // receive buffer] (the split consumer RX); only X1 rows use coherent loads.
+  // launch must be a two-phase overwrite with two sources [X0 = B_local ||
+  // X1 = receive buffer]; only X1 rows use coherent loads.
   const int32_t *ready = nullptr;       // [P] local READY flags (one per source)
   const uint64_t *unit_src = nullptr;   // [n_tasks + n_groups] source masks
   int32_t *wait_epoch = nullptr;

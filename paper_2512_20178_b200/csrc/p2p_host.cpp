@@ -147,16 +147,13 @@ void p2p_setup(Plan &pl, const Alltoallv &xchg) {
   *pl.err_host = 0;
   if (const char *e = getenv("SHIRO_P2P_TIMEOUT_MS")) pl.wait_timeout_ns = atoll(e) * 1000000LL;
   pl.epoch = 0;
-  // the producer branch of a step runs on the highest-priority stream, the
-  // split consumer's LX branch one level below (RX stays on the caller's
-  // stream): pending producer CTAs are dispatched first, then LX, then RX
-  // (whose warps may spin on a late peer)
+  // the producer branch of a step runs on the highest-priority stream:
+  // pending producer CTAs are dispatched before the consumer's (whose warps
+  // may spin on a late peer), so a consumer can never starve its own GPU's
+  // producer
   int lo_prio = 0, hi_prio = 0;
   SHIRO_CK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
   SHIRO_CK(cudaStreamCreateWithPriority(&pl.s_hi, cudaStreamNonBlocking, hi_prio));
-  SHIRO_CK(cudaStreamCreateWithPriority(&pl.s_mid, cudaStreamNonBlocking,
-                                        hi_prio < lo_prio ? hi_prio + 1 : hi_prio));
-  SHIRO_CK(cudaEventCreateWithFlags(&pl.ev_mid, cudaEventDisableTiming));
   if (merged_enabled(pl)) upload_merged(pl);
   SHIRO_CK(cudaEventCreateWithFlags(&pl.ev_fork, cudaEventDisableTiming));
   SHIRO_CK(cudaEventCreateWithFlags(&pl.ev_join, cudaEventDisableTiming));

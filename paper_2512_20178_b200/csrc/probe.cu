@@ -147,11 +147,85 @@ __global__ void __launch_bounds__(256) k_probe_fma(float *__restrict__ out, int 
   out[(int64_t)blockIdx.x * 256 + threadIdx.x] = s;
 }
 
-// HBM copy: float4 grid-stride copy (read + write bytes)
+// HBM copy: float4 grid-stride copy (read + write bytes), 4 loads in flight
+// per thread before the stores
 __global__ void __launch_bounds__(256) k_probe_copy(const float4 *__restrict__ x,
                                                     float4 *__restrict__ y, int64_t n) {
-  for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256)
-    y[i] = __ldcs(x + i);
+  const int64_t stride = (int64_t)gridDim.x * 256;
+  int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  for (; i + 3 * stride < n; i += 4 * stride) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldcs(x + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) __stcs(y + i + u * stride, v[u]);
+  }
+  for (; i < n; i += stride) __stcs(y + i, __ldcs(x + i));
+}
+
+// ---- warp-specialized TMA variant (round 2): in-flight bytes decoupled from
+// warps.  CTA = 1 producer warp + 7 consumer warps, 4 CTAs per SM (32
+// resident warps, as the LDG kernel), an S-stage ring of gather4 tiles
+// (4 rows x 512 B = 2 KB per stage) per CTA: up to 4 x S x 2 KB per SM in
+// flight (S = 24: 192 KB) vs 32 warps x 4 rows x 512 B = 64 KB for LDG.128.
+// Lane 0 of warp 0 issues cp.async.bulk.tensor tile::gather4 into stage
+// q % S after the stage's EMPTY barrier; consumer warp w takes quads
+// q = w, w + 7, ... (FULL barrier with tx bytes), sums its 4 rows and
+// releases the stage.  Each CTA walks a contiguous range of quads.
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
+template <int S>
+__global__ void __launch_bounds__(256) k_probe_gather_tma_ws(const __grid_constant__ CUtensorMap tm,
+                                                             const int32_t *__restrict__ idx,
+                                                             int64_t nquads, int64_t n,
+                                                             float *__restrict__ out) {
+  extern __shared__ __align__(128) float4 ring[];   // S x 4 rows x 32 float4
+  __shared__ __align__(8) uint64_t full[S], empty[S];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t per = (nquads + gridDim.x - 1) / gridDim.x;
+  const int64_t q0 = (int64_t)blockIdx.x * per;
+  const int64_t q1 = (q0 + per < nquads) ? q0 + per : nquads;
+  const int64_t nq = q1 > q0 ? q1 - q0 : 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int64_t q = 0; q < nq; ++q) {
+        const int s = (int)(q % S);
+        if (q >= S) mbar_wait(&empty[s], (uint32_t)(((q / S) - 1) & 1));
+        int r[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int64_t k = 4 * (q0 + q) + i;
+          r[i] = __ldg(idx + (k < n ? k : n - 1));
+        }
+        mbar_expect_tx(&full[s], 4 * 512);
+        tma_gather4(ring + s * 128, &tm, &full[s], r[0], r[1], r[2], r[3]);
+      }
+    }
+    return;
+  }
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t q = warp - 1; q < nq; q += 7) {
+    const int s = (int)(q % S);
+    mbar_wait(&full[s], (uint32_t)((q / S) & 1));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float4 x = ring[s * 128 + i * 32 + lane];
+      acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  reinterpret_cast<float4 *>(out + ((int64_t)blockIdx.x * 7 + warp - 1) * 128)[lane] = acc;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -223,8 +297,41 @@ extern "C" int shiro_probe_copy(const float *x, float *y, int64_t n_floats, void
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t n4 = n_floats / 4;
   if (n4 == 0) return SHIRO_OK;
-  const int64_t grid = std::min<int64_t>((n4 + 255) / 256, (int64_t)sms * 8);
+  const int64_t grid = std::min<int64_t>((n4 + 255) / 256, (int64_t)sms * 16);
   k_probe_copy<<<(unsigned)grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const float4 *>(x), reinterpret_cast<float4 *>(y), n4);
+  return cudaGetLastError() == cudaSuccess ? SHIRO_OK : SHIRO_E_CUDA;
+}
+
+extern "C" int shiro_probe_gather_tma_ws(const float *X, int64_t x_rows, int32_t N,
+                                         const int32_t *idx, int64_t n_idx, float *out,
+                                         int32_t stages, int32_t ctas, void *stream) {
+  if (!X || !idx || !out || n_idx < 4 || n_idx % 4 || N != 128 || x_rows < 1 || ctas < 1)
+    return SHIRO_E_ARG;
+  if (stages != 8 && stages != 16 && stages != 24) return SHIRO_E_ARG;
+  auto enc = encode_fn();
+  if (!enc) return SHIRO_E_CUDA;
+  CUtensorMap tm;
+  const cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)x_rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)N * sizeof(float)};
+  const cuuint32_t box[2] = {(cuuint32_t)N, 1};
+  const cuuint32_t estr[2] = {1, 1};
+  if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(X), dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return SHIRO_E_CUDA;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t smem = (size_t)stages * 4 * 512;
+  const int64_t nq = n_idx / 4;
+#define SHIRO_WS(S_)                                                                            \
+  do {                                                                                          \
+    cudaFuncSetAttribute(k_probe_gather_tma_ws<S_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                         (int)smem);                                                            \
+    k_probe_gather_tma_ws<S_><<<ctas, 256, smem, s>>>(tm, idx, nq, n_idx, out);                 \
+  } while (0)
+  if (stages == 8) SHIRO_WS(8);
+  else if (stages == 16) SHIRO_WS(16);
+  else SHIRO_WS(24);
+#undef SHIRO_WS
   return cudaGetLastError() == cudaSuccess ? SHIRO_OK : SHIRO_E_CUDA;
 }

@@ -36,8 +36,6 @@ Plan::~Plan() {
     if (stage) cudaFree(stage);
     if (vspace) cudaFree(vspace);
     if (merged_ops) cudaFree(merged_ops);
-    if (s_mid) cudaStreamDestroy(s_mid);
-    if (ev_mid) cudaEventDestroy(ev_mid);
     for (cudaEvent_t e : {ev_in, ev_comp, ev_out})
       if (e) cudaEventDestroy(e);
     if (h2d_s) cudaStreamDestroy(h2d_s);
@@ -101,6 +99,8 @@ struct SplitHost {
   std::vector<uint8_t> roff;
   std::vector<int2> cv;
   std::vector<uint64_t> unit_src;   // per unit (tasks, then groups): source mask
+  std::vector<int32_t> vsrc;        // refresh map in cv order (two-phase ops permute)
+  std::vector<int64_t> long_mid;    // two-phase ops: first remote nonzero of each long row
   bool hot = false;
 };
 
@@ -177,7 +177,35 @@ SplitHost make_split(const HostCsr &c, int N) {
       sum += deg(t);
       ++t;
     }
-    s.groups.push_back(RowGroup{c.rp[r0], c.rp[t], (int32_t)r0, (int32_t)t});
+    s.groups.push_back(RowGroup{c.rp[r0], c.rp[t], c.rp[t], (int32_t)r0, (int32_t)t});
+  }
+  if (!c.mid.empty()) {
+    // two-phase op: inside each group, every row's local part (row order),
+    // then every row's remote part (row order); kmid between them
+    if ((int64_t)c.mid.size() != c.nrows) throw Error(SHIRO_E_INTERNAL, "two-phase map size");
+    s.vsrc = c.vsrc;
+    std::vector<int2> tcv;
+    std::vector<uint8_t> troff;
+    std::vector<int32_t> tvs;
+    for (RowGroup &g : s.groups) {
+      tcv.clear(); troff.clear(); tvs.clear();
+      for (int ph = 0; ph < 2; ++ph) {
+        if (ph == 1) g.kmid = g.k0 + (int64_t)tcv.size();
+        for (int32_t r = g.r0; r < g.r1; ++r) {
+          const int64_t a = ph == 0 ? c.rp[r] : c.rp[r] + c.mid[r];
+          const int64_t b = ph == 0 ? c.rp[r] + c.mid[r] : c.rp[r + 1];
+          for (int64_t k = a; k < b; ++k) {
+            tcv.push_back(s.cv[k]);
+            troff.push_back(s.roff[k]);
+            if (!s.vsrc.empty()) tvs.push_back(s.vsrc[k]);
+          }
+        }
+      }
+      std::copy(tcv.begin(), tcv.end(), s.cv.begin() + g.k0);
+      std::copy(troff.begin(), troff.end(), s.roff.begin() + g.k0);
+      if (!s.vsrc.empty()) std::copy(tvs.begin(), tvs.end(), s.vsrc.begin() + g.k0);
+    }
+    for (int32_t t : s.long_row) s.long_mid.push_back(c.rp[t] + c.mid[t]);
   }
   if (!c.src_bounds.empty()) {
     // per-unit source masks (fused exchange consumer): the sources whose
@@ -210,7 +238,7 @@ SplitHost make_split(const HostCsr &c, int N) {
 }
 
 struct SpmmLayout {
-  size_t rp, cv, roff, out, tl, lrow, lfirst, cnt, scratch, grp, usrc, vsrc;
+  size_t rp, cv, roff, out, tl, lrow, lfirst, cnt, scratch, grp, usrc, vsrc, lmid;
   SplitHost sp;
   bool has_out, has_usrc, has_vsrc;
 };
@@ -234,7 +262,8 @@ SpmmLayout layout_spmm(Arena &ar, const HostCsr &c, int N) {
   L.has_vsrc = !c.vsrc.empty();
   if (L.has_vsrc && (int64_t)c.vsrc.size() != c.nnz())
     throw Error(SHIRO_E_INTERNAL, "refresh map size");
-  L.vsrc = put(ar, c.vsrc);
+  L.vsrc = put(ar, L.sp.vsrc.empty() ? c.vsrc : L.sp.vsrc);
+  L.lmid = put(ar, L.sp.long_mid);
   return L;
 }
 
@@ -260,6 +289,7 @@ DevSpmm bind_spmm(char *base, const SpmmLayout &L, const HostCsr &c, int N) {
   a.unit_src = L.has_usrc ? reinterpret_cast<const uint64_t *>(base + L.usrc) : nullptr;
   d.nnz = c.nnz();
   d.vsrc = L.has_vsrc ? reinterpret_cast<const int32_t *>(base + L.vsrc) : nullptr;
+  a.long_mid = c.mid.empty() ? nullptr : reinterpret_cast<const int64_t *>(base + L.lmid);
   return d;
 }
 
@@ -451,52 +481,42 @@ void upload_prod(Plan &pl, const std::vector<int32_t> &pack_src,
   }
 }
 
-// Split consumer of the fused exchange: LX = the rows of
-// A_diag without remote entries (overwrite), RX = every row with remote
-// entries, computed whole: its diagonal nonzeros (columns in B_local) then
-// its A_rem entries (columns shifted by M into the receive buffer), overwrite.
-// Disjoint output rows, so LX runs while RX waits for its sources.
+// Two-phase consumer of the fused exchange: every local
+// row t, its diagonal nonzeros (columns in B_local) then its A_rem entries
+// (column-based entries and unit-weight partials, columns shifted by M into
+// the receive buffer); mid[t] = number of diagonal nonzeros.  Overwrite, one
+// store per row in phase A, read-modify-write in phase B only for rows with
+// remote entries.
 void upload_merged(Plan &pl) {
   const int64_t M = pl.M;
   const HostCsr &ad = pl.A_diag, &ar = pl.A_rem;
-  std::vector<uint8_t> has_rem(M, 0);
-  for (int32_t t : ar.out_row) has_rem[t] = 1;
+  std::vector<int64_t> rem_of(M, -1);
+  for (int64_t i = 0; i < ar.nrows; ++i) rem_of[ar.out_row[i]] = i;
   const bool refresh = !ad.vsrc.empty();
-  HostCsr lx, rx;
-  lx.hot_rows = M;
+  HostCsr cx;
+  cx.nrows = M;
+  cx.mid.resize(M);
+  cx.col.reserve(ad.nnz() + ar.nnz());
   for (int64_t t = 0; t < M; ++t) {
-    if (has_rem[t]) continue;
     for (int64_t k = ad.rp[t]; k < ad.rp[t + 1]; ++k) {
-      lx.col.push_back(ad.col[k]);
-      lx.val.push_back(ad.val[k]);
-      if (refresh) lx.vsrc.push_back(ad.vsrc[k]);
+      cx.col.push_back(ad.col[k]);
+      cx.val.push_back(ad.val[k]);
+      if (refresh) cx.vsrc.push_back(ad.vsrc[k]);
     }
-    lx.rp.push_back((int64_t)lx.col.size());
-    lx.out_row.push_back((int32_t)t);
+    cx.mid[t] = (int32_t)(ad.rp[t + 1] - ad.rp[t]);
+    if (const int64_t i = rem_of[t]; i >= 0)
+      for (int64_t k = ar.rp[i]; k < ar.rp[i + 1]; ++k) {
+        cx.col.push_back((int32_t)(M + ar.col[k]));
+        cx.val.push_back(ar.val[k]);
+        if (refresh) cx.vsrc.push_back(ar.vsrc.empty() ? -1 : ar.vsrc[k]);
+      }
+    cx.rp.push_back((int64_t)cx.col.size());
   }
-  lx.nrows = (int64_t)lx.out_row.size();
-  for (int64_t i = 0; i < ar.nrows; ++i) {
-    const int64_t t = ar.out_row[i];
-    for (int64_t k = ad.rp[t]; k < ad.rp[t + 1]; ++k) {
-      rx.col.push_back(ad.col[k]);
-      rx.val.push_back(ad.val[k]);
-      if (refresh) rx.vsrc.push_back(ad.vsrc[k]);
-    }
-    for (int64_t k = ar.rp[i]; k < ar.rp[i + 1]; ++k) {
-      rx.col.push_back((int32_t)(M + ar.col[k]));
-      rx.val.push_back(ar.val[k]);
-      if (refresh) rx.vsrc.push_back(ar.vsrc.empty() ? -1 : ar.vsrc[k]);
-    }
-    rx.rp.push_back((int64_t)rx.col.size());
-    rx.out_row.push_back((int32_t)t);
-  }
-  rx.nrows = (int64_t)rx.out_row.size();
-  for (int64_t b : pl.recv_off) rx.src_bounds.push_back(M + b);   // per-unit source masks
-  if ((int64_t)rx.col.size() + M > 0x7fffffffLL || M + pl.recv_rows > 0x7fffffffLL)
-    throw Error(SHIRO_E_ARG, "merged consumer: more than 2^31 source rows");
+  for (int64_t b : pl.recv_off) cx.src_bounds.push_back(M + b);   // per-unit source masks
+  if (M + pl.recv_rows > 0x7fffffffLL)
+    throw Error(SHIRO_E_ARG, "two-phase consumer: more than 2^31 source rows");
   Arena ar2;
-  SpmmLayout L1 = layout_spmm(ar2, lx, pl.N);
-  SpmmLayout L2 = layout_spmm(ar2, rx, pl.N);
+  SpmmLayout L = layout_spmm(ar2, cx, pl.N);
   if (pl.merged_ops) cudaFree(pl.merged_ops);
   SHIRO_CK(cudaMalloc(&pl.merged_ops, std::max<size_t>(ar2.total, 256)));
   SHIRO_CK(cudaMemset(pl.merged_ops, 0, std::max<size_t>(ar2.total, 256)));
@@ -504,22 +524,17 @@ void upload_merged(Plan &pl) {
   for (const auto &it : ar2.items)
     if (it.src && it.bytes)
       SHIRO_CK(cudaMemcpy(base + it.off, it.src, it.bytes, cudaMemcpyHostToDevice));
-  pl.d_lx = bind_spmm(base, L1, lx, pl.N);
-  pl.d_rx = bind_spmm(base, L2, rx, pl.N);
-  pl.refresh_ops.push_back(&pl.d_lx);
-  pl.refresh_ops.push_back(&pl.d_rx);
+  pl.d_cx = bind_spmm(base, L, cx, pl.N);
+  pl.refresh_ops.push_back(&pl.d_cx);
   pl.info.dev_bytes += (int64_t)ar2.total;
-  auto distinct = [](const std::vector<int32_t> &ids) {
-    std::vector<int32_t> v(ids);
-    std::sort(v.begin(), v.end());
-    return (int64_t)(std::unique(v.begin(), v.end()) - v.begin());
-  };
-  pl.info.op_nnz[SHIRO_OP_LOCAL] = lx.nnz();
-  pl.info.op_rows[SHIRO_OP_LOCAL] = lx.nrows;
-  pl.info.op_src_rows[SHIRO_OP_LOCAL] = distinct(lx.col);
-  pl.info.op_nnz[SHIRO_OP_REMOTE] = rx.nnz();
-  pl.info.op_rows[SHIRO_OP_REMOTE] = rx.nrows;
-  pl.info.op_src_rows[SHIRO_OP_REMOTE] = distinct(rx.col);
+  // the consumer carries the local (K1) and remote (K2 + K5) work of a step
+  std::vector<int32_t> src(cx.col);
+  std::sort(src.begin(), src.end());
+  pl.info.op_nnz[SHIRO_OP_LOCAL] = ad.nnz();
+  pl.info.op_rows[SHIRO_OP_LOCAL] = M;
+  pl.info.op_nnz[SHIRO_OP_REMOTE] = cx.nnz();
+  pl.info.op_rows[SHIRO_OP_REMOTE] = M;
+  pl.info.op_src_rows[SHIRO_OP_REMOTE] = (int64_t)(std::unique(src.begin(), src.end()) - src.begin());
   pl.merged = true;
 }
 
@@ -826,11 +841,11 @@ void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
   const int par = pl.dbuf ? pl.step_parity : 0;
   float *rb = par ? pl.recv_buf2 : pl.recv_buf;
   if (pl.merged) {
-    // split consumer: producer (s_hi) || LX (s_mid) || RX (s, per-source waits)
+    // two-phase consumer: producer (s_hi) || CX (s: K1 parts, then per-source
+    // waits, then K2 + K5 parts)
     rec(0, s);
     SHIRO_CK(cudaEventRecord(pl.ev_fork, s));
     SHIRO_CK(cudaStreamWaitEvent(pl.s_hi, pl.ev_fork, 0));
-    SHIRO_CK(cudaStreamWaitEvent(pl.s_mid, pl.ev_fork, 0));
     if (!pl.dbuf)
       launches += launch_wait(pl.xflags + P, P, ep_sig, 0, err, pl.wait_timeout_ns, pl.s_hi);
     DevSpmm prod = pl.d_prod;
@@ -840,26 +855,22 @@ void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
     launches += launch_signal(pl.ready_ptrs, P - 1, ep_sig, 1, true, pl.s_hi);
     rec(2, pl.s_hi);
     SHIRO_CK(cudaEventRecord(pl.ev_join, pl.s_hi));
-    launches += run_spmm(pl.d_lx, B, pl.M, nullptr, C, false, pl.s_mid);
-    rec(3, pl.s_mid);
-    SHIRO_CK(cudaEventRecord(pl.ev_mid, pl.s_mid));
-    if (pl.d_rx.a.n_groups + pl.d_rx.a.n_tasks > 0) {
-      DevSpmm rx = pl.d_rx;
-      rx.a.ready = pl.xflags;
-      rx.a.wait_epoch = ep_wait;
-      rx.a.wait_err = err;
-      rx.a.done_ctr = done;
-      rx.a.wait_all = P;
-      rx.a.wait_timeout_ns = pl.wait_timeout_ns;
-      launches += run_spmm(rx, B, pl.M, rb, C, false, s);
-    } else {   // nothing received: the step-end barrier alone
+    if (pl.d_cx.a.n_groups + pl.d_cx.a.n_tasks > 0) {
+      DevSpmm cx = pl.d_cx;
+      cx.a.ready = pl.xflags;
+      cx.a.wait_epoch = ep_wait;
+      cx.a.wait_err = err;
+      cx.a.done_ctr = done;
+      cx.a.wait_all = P;
+      cx.a.wait_timeout_ns = pl.wait_timeout_ns;
+      launches += run_spmm(cx, B, pl.M, rb, C, false, s);
+    } else {   // no local rows: the step-end barrier alone
       launches += launch_wait(pl.xflags, P, ep_wait, 1, err, pl.wait_timeout_ns, s, true);
     }
-    rec(4, s);
-    SHIRO_CK(cudaStreamWaitEvent(s, pl.ev_mid, 0));
+    rec(3, s);
     SHIRO_CK(cudaStreamWaitEvent(s, pl.ev_join, 0));
     if (!pl.dbuf) launches += launch_signal(pl.consumed_ptrs, P - 1, ep_wait, 0, false, s);
-    rec(5, s);
+    rec(4, s);
     SHIRO_CK(cudaMemcpyAsync(pl.err_host, err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     pl.last_launches = launches;
     pl.prof_used = 5;
@@ -1644,9 +1655,8 @@ int shiro_spmm_loopback(shiro_plan_t plan, const float *B, float *C, void *strea
       }
       for (int r = 0; r < P; ++r) {
         Plan &pl = *plan->ranks[r];
-        if (pl.merged) {   // split consumer: LX, then RX over [B_local || receive buffer]
-          launches += run_spmm(pl.d_lx, Bp(r), pl.M, nullptr, Cp(r), false, s);
-          launches += run_spmm(pl.d_rx, Bp(r), pl.M, pl.recv_buf, Cp(r), false, s);
+        if (pl.merged) {   // two-phase consumer over [B_local || receive buffer]
+          launches += run_spmm(pl.d_cx, Bp(r), pl.M, pl.recv_buf, Cp(r), false, s);
         } else {
           launches += stage_local(pl, Bp(r), Cp(r), s);
           launches += stage_recv(pl, Cp(r), s);
@@ -1766,15 +1776,14 @@ int shiro_stage_times(shiro_plan_t plan, double *ms) {
       return;
     }
     if (pl.prof_used == 5) {
-      // split consumer (default fused exchange): PARTIAL = producer (K4 + K3
-      // -> peers), EXCHANGE = its READY signal, LOCAL = LX, REMOTE = RX (rows
-      // with remote entries computed whole, including its per-source waits);
-      // all measured from the step's start (the three branches overlap)
+      // two-phase consumer (default fused exchange): PARTIAL = producer (K4
+      // + K3 -> peers), EXCHANGE = its READY signal, REMOTE = the consumer
+      // launch (K1 + K2 + K5 with its per-source waits), from the step's
+      // start (the branches overlap); LOCAL is not separable (0)
       ms[SHIRO_STAGE_PARTIAL] = el(0, 1);
       ms[SHIRO_STAGE_EXCHANGE] = el(1, 2);
-      ms[SHIRO_STAGE_LOCAL] = el(0, 3);
-      ms[SHIRO_STAGE_REMOTE] = el(0, 4);
-      ms[SHIRO_STAGE_TOTAL] = el(0, 5);
+      ms[SHIRO_STAGE_REMOTE] = el(0, 3);
+      ms[SHIRO_STAGE_TOTAL] = el(0, 4);
       return;
     }
     if (pl.prof_used == 3) {

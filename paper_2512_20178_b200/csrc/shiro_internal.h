@@ -60,6 +60,8 @@ struct HostCsr {
   std::vector<int64_t> src_bounds;   // non-empty: source s owns columns
                                      // [src_bounds[s], src_bounds[s+1]) -> per-unit masks
   int64_t hot_rows = -1;        // >= 0: number of source rows (hot/cold L2 marks)
+  std::vector<int32_t> mid;     // two-phase op: per row, the number of leading
+                                // (local-part) nonzeros; empty = one phase
   int64_t nnz() const { return (int64_t)col.size(); }
 };
 
@@ -191,15 +193,14 @@ struct Plan {
   // carries the local rows into C (K1)
   DevSpmm d_prod;
   void *prod_ops = nullptr;
-  // split consumer of the fused exchange (default): rows without remote
-  // entries (K1 only, "LX") and rows with remote entries computed whole from
-  // [B_local || receive buffer] ("RX": K1 + K2 + K5 of those rows, per-source
-  // waits), disjoint output rows -> the two launches run concurrently
+  // two-phase consumer of the fused exchange (default, "CX"): every local row
+  // from [B_local || receive buffer]; per work unit its local parts (K1)
+  // first, then -- after the READY of the sources it reads -- its remote
+  // parts (K2 + K5), so K1 overlaps the producer and each peer's rows are
+  // consumed as they land
   bool merged = false;
-  DevSpmm d_lx, d_rx;
+  DevSpmm d_cx;
   void *merged_ops = nullptr;
-  cudaStream_t s_mid = nullptr;       // LX branch (priority between producer and RX)
-  cudaEvent_t ev_mid = nullptr;
   cudaStream_t s_hi = nullptr;        // producer branch of a step (high priority)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int32_t *err_host = nullptr;        // pinned copy of the error flag
@@ -291,7 +292,7 @@ void upload_prod(Plan &plan, const std::vector<int32_t> &pack_src,
 // value refresh of a plan's device ops from the new value space V (host)
 void refresh_device(Plan &plan, const std::vector<float> &V, cudaStream_t s);
 void plan_drop_host(Plan &plan);
-// build + upload the split consumer (LX, RX) of the fused exchange
+// build + upload the two-phase consumer (CX) of the fused exchange
 void upload_merged(Plan &plan);
 bool merged_enabled(const Plan &plan);
 void p2p_release(Plan &plan);

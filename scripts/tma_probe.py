@@ -42,19 +42,29 @@ def timeit(fn):
 
 
 def run(name, X, idx):
+    idx = idx[: idx.numel() // 4 * 4]
     n = idx.numel()
     outs = {}
     variants = [("ldg", lambda o: sh.probe_gather(X, idx, o, CHUNK))]
     for st in (2, 4, 8):
         variants.append((f"tma_s{st}", lambda o, st=st: sh.probe_gather_tma(X, idx, o, CHUNK, st)))
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    for st in (8, 16, 24):      # warp-specialized ring, 4 CTAs x 8 warps per SM (round 2)
+        variants.append((f"ws_s{st}", lambda o, st=st: sh.probe_gather_tma_ws(X, idx, o, st, 4 * sms)))
     for vname, fn in variants:
-        out = torch.empty(((n + CHUNK - 1) // CHUNK, N), device="cuda")
+        rows = max((n + CHUNK - 1) // CHUNK, 4 * sms * 7)
+        out = torch.zeros((rows, N), device="cuda")
         ms = timeit(lambda: fn(out))
         outs[vname] = out
         print(f"{name:28s} {vname:7s} {ms:8.4f} ms  {n * 4 * N / ms / 1e6:9.1f} GB/s", flush=True)
     ref = outs["ldg"]
+    tot = float(ref.double().sum())
     for k, v in outs.items():
-        if not torch.equal(v, ref):
+        if k.startswith("ws_"):        # different partial sums: compare totals
+            t = float(v.double().sum())
+            if abs(t - tot) > 1e-4 * abs(tot):
+                print(f"  MISMATCH {k}: total {t:.6e} vs {tot:.6e}", flush=True)
+        elif not torch.equal(v, ref):
             print(f"  MISMATCH {k}: max diff {float((v - ref).abs().max()):.3e}", flush=True)
 
 
