@@ -599,7 +599,17 @@ def measure(cfg_name, args, ctx, primary):
                 "achieved_gbs_over_producer": round(gbs, 1) if gbs else None,
                 "peak_gbs": nvl_bw, "frac": round(gbs / nvl_bw, 4) if gbs and nvl_bw else None}
 
+    # N3: one value refresh of the plan (same values; collective), timed on
+    # the host around the call (the refresh returns after the device update)
+    barrier()
+    t0 = time.perf_counter()
+    plan.update_values(val_l, row_ptr=rp_l, col=col_l, stream=stream)
+    t_ref = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_ref, op=dist.ReduceOp.MAX)
+
     res = {
+        "refresh_seconds": round(float(t_ref.item()), 4),
         "config": cfg, "value": value, "ms": ms, "nnz": nnz, "info": info, "roofline": roof,
         "roofline_step": step_roof, "gather": gather, "exchange": exch, "launches": launches,
         "stage_ms": stage_ms, "per_rank": per_rank, "step_ms": step_ms,
@@ -625,7 +635,8 @@ def summary(r):
             "ms_per_step": round(r["ms"], 5), "roofline": r["roofline"],
             "roofline_step": r["roofline_step"], "exchange": r["exchange"],
             "stages_ms": {k: round(v, 5) for k, v in r["stage_ms"].items()},
-            "bytes": r["bytes"], "plan_seconds": round(r["info"]["plan_seconds"], 3)}
+            "bytes": r["bytes"], "plan_seconds": round(r["info"]["plan_seconds"], 3),
+            "refresh_seconds": r["refresh_seconds"]}
 
 
 # ----------------------------------------------------------------- main
@@ -807,6 +818,7 @@ def main():
                         "p10": round(float(np.percentile(step_ms, 10)), 5),
                         "p90": round(float(np.percentile(step_ms, 90)), 5)},
             "plan_seconds": round(main_r["info"]["plan_seconds"], 3),
+            "refresh_seconds": main_r["refresh_seconds"],
             "also": others,
         }
         print(json.dumps(out), flush=True)
