@@ -76,11 +76,17 @@ __device__ __forceinline__ float4 ldB(const float4 *p, bool hot, bool coh) {
                  : "l"(p));
   } else if (HINT == 0) {
     v = __ldg(p);
-  } else {
-    const uint64_t pol = (HINT == 2 || hot) ? pol_last() : pol_first();
+  } else if (HINT == 2 || hot) {
+    // the policy operand lives in a uniform register: one load per constant
+    // policy (a per-row select would make the compiler waterfall over lanes);
+    // `hot` is uniform across the lane group, so this branch never diverges
     asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
                  : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                 : "l"(p), "l"(pol));
+                 : "l"(p), "l"(pol_last()));
+  } else {
+    asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p), "l"(pol_first()));
   }
   return v;
 }
