@@ -63,13 +63,19 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
                : "memory");
 }
+// the retry loop is C++ (no label inside inline asm: a kernel that inlines
+// the wait twice must not end up with two branch targets of the same name)
 __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra W;\n}\n" ::"r"(smem_u32(b)),
-      "r"(parity)
-      : "memory");
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  }
 }
 __device__ __forceinline__ void tma_gather4(void *dst, const CUtensorMap *tm, uint64_t *bar, int r0,
                                             int r1, int r2, int r3) {
@@ -200,7 +206,10 @@ __global__ void __launch_bounds__(256) k_probe_gather_tma_ws(const __grid_consta
     if (lane == 0) {
       for (int64_t q = 0; q < nq; ++q) {
         const int s = (int)(q % S);
-        if (q >= S) mbar_wait(&empty[s], (uint32_t)(((q / S) - 1) & 1));
+        if (q >= S) {
+          mbar_wait(&empty[s], (uint32_t)(((q / S) - 1) & 1));
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // consumers' reads -> async writes
+        }
         int r[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
