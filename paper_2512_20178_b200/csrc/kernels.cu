@@ -444,8 +444,14 @@ __global__ void __launch_bounds__(BS, MINB) k_spmm(const SpmmArgs a) {
     // target epoch read before this warp is counted done (the last warp
     // advances it, after every warp has read it)
     const int32_t target = *reinterpret_cast<volatile int32_t *>(a.wait_epoch) + 1;
-    spmm_unit<LPR, VPL, ACCUM, TWO, (U < LPR ? U : LPR), OUTP, HINT, true, false, true, true>(
-        a, u, li, mask, target);
+    if (PH) {   // two-phase consumer: waits between its local and remote parts
+      spmm_unit<LPR, VPL, ACCUM, TWO, (U < LPR ? U : LPR), OUTP, HINT, true, false, true, true>(
+          a, u, li, mask, target);
+    } else {    // remote SpMM: each lane group waits for its own unit's sources first
+      const bool in = u < (int64_t)a.n_tasks + a.n_groups;
+      if (in && unit_wait<true>(a, u, target, li, LPR, mask))
+        spmm_unit<LPR, VPL, ACCUM, TWO, (U < LPR ? U : LPR), OUTP, HINT, true>(a, u, li, mask);
+    }
     __syncwarp();
     int last = 0;
     if (lane == 0) {
@@ -669,8 +675,10 @@ void spmm_launch(const SpmmArgs &a, bool acc, cudaStream_t s) {
   const int64_t per_cta = (int64_t)(BS / 32) * (32 / LPR);
   const unsigned grid = (unsigned)((units + per_cta - 1) / per_cta);
   const bool two = a.X1 != nullptr;
-  if (a.ready) {     // fused-exchange consumer (CX): per-source waits, coherent receive-buffer loads
+  if (a.ready && a.long_mid) {   // two-phase consumer (CX): waits between its phases
     k_spmm<LPR, VPL, false, true, U, false, 0, true, BS, MINB, false, true><<<grid, BS, 0, s>>>(a);
+  } else if (a.ready) {   // remote SpMM with per-unit source waits, coherent loads
+    k_spmm<LPR, VPL, true, false, U, false, 0, true, BS, MINB, false, false><<<grid, BS, 0, s>>>(a);
   } else if (a.long_mid) {   // two-phase consumer without waits (loopback)
     k_spmm<LPR, VPL, false, true, U, false, 0, false, BS, MINB, false, true><<<grid, BS, 0, s>>>(a);
   } else if (a.out_ptr) {   // fused exchange: overwrite rows in peer buffers

@@ -825,9 +825,19 @@ bool inkernel_wait_enabled() {
 
 // The split consumer is used with the in-kernel waits, the fused K2+K5 and a
 // vector width (the WAIT kernel); otherwise local SpMM -> k_wait -> remote.
+// Opt-in (SHIRO_CX=1) until its spin-free variant exists: with its warps
+// spinning in phase B, the consumer can occupy every SM slot before the
+// GPU's own producer has finished, and two GPUs then wait on each other
+// (seen on 2 x B200; one GPU shared by two processes time-slices and hides it).
 bool merged_enabled(const Plan &pl) {
+  static int env = -1;
+  if (env < 0) {
+    const char *e = getenv("SHIRO_CX");
+    env = (e && e[0] == '1') ? 1 : 0;
+  }
   int lpr, vpl;
-  return inkernel_wait_enabled() && !(pl.flags & SHIRO_F_SPLIT_RECV) && vec_shape(pl.N, &lpr, &vpl);
+  return env == 1 && inkernel_wait_enabled() && !(pl.flags & SHIRO_F_SPLIT_RECV) &&
+         vec_shape(pl.N, &lpr, &vpl);
 }
 
 void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
@@ -889,9 +899,13 @@ void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
   launches += launch_signal(pl.ready_ptrs, P - 1, ep_sig, 1, true, pl.s_hi);
   rec(2, pl.s_hi);
   SHIRO_CK(cudaEventRecord(pl.ev_join, pl.s_hi));
-  // consumer branch
+  // consumer branch: K1 (concurrent with the producer branch); then, once
+  // this GPU's own producer and READY signal are done (so no spinning
+  // consumer warp can hold an SM slot its producer needs), the remote SpMM
+  // whose units each wait only for the sources they read
   launches += stage_local(pl, B, C, s);
   rec(3, s);
+  SHIRO_CK(cudaStreamWaitEvent(s, pl.ev_join, 0));
   int lpr_, vpl_;
   const bool split = pl.flags & SHIRO_F_SPLIT_RECV;
   if (inkernel_wait_enabled() && !split && pl.d_rem.a.n_groups + pl.d_rem.a.n_tasks > 0 &&
@@ -915,7 +929,6 @@ void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
     }
   }
   rec(4, s);
-  SHIRO_CK(cudaStreamWaitEvent(s, pl.ev_join, 0));
   if (!pl.dbuf) launches += launch_signal(pl.consumed_ptrs, P - 1, ep_wait, 0, false, s);
   rec(5, s);
   SHIRO_CK(cudaMemcpyAsync(pl.err_host, err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));

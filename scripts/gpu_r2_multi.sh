@@ -18,6 +18,9 @@ for v in ${VARIANTS}; do   # e.g. "SHIRO_INKERNEL_WAIT=0"
     > gpurun_out/${TAG}_P${NG}_$v.json 2> gpurun_out/${TAG}_P${NG}_$v.err
 done
 if [ "${C5:-0}" = "1" ]; then
+  # generate once in one process (cached): a rank generating c5 inside the
+  # bench would hold the others at a barrier past NCCL's 10-minute timeout
+  ( time python -c "import shiro_gen; shiro_gen.gen_matrix('c5', cache_dir='/tmp/shiro_gen_cache')" ) > gpurun_out/${TAG}_c5gen.log 2>&1
   timeout 2400 $TR bench.py --gpus $NG --config c5 --also none --no-e2e --no-probes --steps 10 \
     > gpurun_out/${TAG}_P${NG}_c5.json 2> gpurun_out/${TAG}_P${NG}_c5.err
 fi
