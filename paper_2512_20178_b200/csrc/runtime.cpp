@@ -830,13 +830,9 @@ bool inkernel_wait_enabled() {
 // GPU's own producer has finished, and two GPUs then wait on each other
 // (seen on 2 x B200; one GPU shared by two processes time-slices and hides it).
 bool merged_enabled(const Plan &pl) {
-  static int env = -1;
-  if (env < 0) {
-    const char *e = getenv("SHIRO_CX");
-    env = (e && e[0] == '1') ? 1 : 0;
-  }
+  const char *e = getenv("SHIRO_CX");     // read at plan time
   int lpr, vpl;
-  return env == 1 && inkernel_wait_enabled() && !(pl.flags & SHIRO_F_SPLIT_RECV) &&
+  return e && e[0] == '1' && inkernel_wait_enabled() && !(pl.flags & SHIRO_F_SPLIT_RECV) &&
          vec_shape(pl.N, &lpr, &vpl);
 }
 

@@ -126,6 +126,23 @@ def test_loopback_random_integer_exact(P, flags):
     assert np.array_equal(C.astype(np.float64), oracle.spmm_ref(row_ptr, col, val, B))
 
 
+@pytest.mark.parametrize("P", [2, 3, 8])
+@pytest.mark.parametrize("N", [32, 64, 128])
+def test_loopback_two_phase_consumer_exact(P, N, monkeypatch):
+    """The opt-in two-phase consumer CX (SHIRO_CX=1):
+    per row group [local parts || remote parts], hub rows split at the local
+    / remote boundary; integer data exact."""
+    monkeypatch.setenv("SHIRO_CX", "1")
+    rng = np.random.default_rng(P * 7 + N)
+    n = 2500
+    row_ptr, col = hub_matrix(rng, n, 2000, 0.004)
+    val = rng.integers(1, 5, col.size).astype(np.float32)
+    B = rng.integers(0, 8, (n, N)).astype(np.float32)
+    part = oracle.uniform_partition(n, P)
+    C, _ = run_loopback(n, part, row_ptr, col, val, B)
+    assert np.array_equal(C.astype(np.float64), oracle.spmm_ref(row_ptr, col, val, B))
+
+
 @pytest.mark.parametrize("cfg,P", [("c1", 1), ("c1", 2), ("c2", 1), ("c2", 2), ("c2", 4),
                                    ("c2", 8)])
 def test_config_parity(cfg, P):
