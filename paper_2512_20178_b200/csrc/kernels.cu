@@ -224,8 +224,32 @@ __device__ __forceinline__ bool unit_wait(const SpmmArgs &a, int64_t u, int32_t 
   return wait_sources(a.ready, need, target, a.wait_err, a.wait_timeout_ns, li, lanes, mask);
 }
 
+// Non-blocking readiness of unit u's sources (one poll per lane group).
+__device__ __forceinline__ bool sources_ready(const SpmmArgs &a, int64_t u, int32_t target, int li,
+                                              int lanes, unsigned mask) {
+  const uint64_t need = a.unit_src[u];
+  bool ok = true;
+  for (int s = li; s < 64; s += lanes)
+    if ((need >> s) & 1ull) {
+      int32_t v;
+      asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(a.ready + s) : "memory");
+      ok = ok && v >= target;
+    }
+  return __all_sync(mask, ok);
+}
+
+// Push unit u to the deferred list of the two-phase consumer (lane 0 of the group).
+__device__ __forceinline__ void defer_unit(const SpmmArgs &a, int64_t u, int li) {
+  if (li == 0) a.defer_list[atomicAdd(a.defer_n, 1)] = (int32_t)u;
+}
+
+// STAGE (two-phase ops, PH): 0 = both phases inline (waiting in between when
+// WAIT); 1 = phase A, then phase B only if the unit's sources are already
+// READY, else the unit is deferred (a hub chunk parks its partial in its
+// scratch row) -- never spins; 2 = the deferred continuation: phase B after
+// waiting for the sources (launched after this GPU's producer and READY).
 template <int LPR, int VPL, bool ACCUM, bool TWO, int U, bool OUTP, int HINT, bool COH,
-          bool PF = false, bool PH = false, bool WAIT = false>
+          bool PF = false, bool PH = false, bool WAIT = false, int STAGE = 0>
 __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, const int li,
                                           const unsigned mask, const int32_t target = 0) {
   float4 acc[VPL];
@@ -263,9 +287,24 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
         }
       }
     };
-    walk(kb, kmid);
-    if (PH && kmid < ke && unit_wait<WAIT>(a, u, target, li, LPR, mask)) walk(kmid, ke);
     float4 *sp = reinterpret_cast<float4 *>(a.scratch + u * (int64_t)a.N);
+    if (STAGE == 2) {       // deferred continuation: the parked phase-A partial
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) acc[q] = __ldcg(sp + li + q * LPR);
+    } else {
+      walk(kb, kmid);
+    }
+    if (PH && kmid < ke) {
+      if (STAGE == 1 && !sources_ready(a, u, target, li, LPR, mask)) {
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) __stcg(sp + li + q * LPR, acc[q]);
+        defer_unit(a, u, li);
+        return;
+      }
+      if (STAGE == 2 ? unit_wait<true>(a, u, target, li, LPR, mask)
+                     : (STAGE == 1 || unit_wait<WAIT>(a, u, target, li, LPR, mask)))
+        walk(kmid, ke);
+    }
 #pragma unroll
     for (int q = 0; q < VPL; ++q) __stcg(sp + li + q * LPR, acc[q]);
     __threadfence();
@@ -351,7 +390,7 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
     }
     ++cur;
   };
-  for (int64_t base = g.k0; base < kend; base += LPR) {
+  for (int64_t base = g.k0; STAGE != 2 && base < kend; base += LPR) {
     const int64_t k = base + li;
     int2 cv = make_int2(0, 0);
     int ro = 0;
@@ -376,12 +415,20 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
       }
     }
   }
-  while (cur < nrows) flush();              // last row and trailing empty rows
+  if (STAGE != 2)
+    while (cur < nrows) flush();            // last row and trailing empty rows
   if (!PH || g.kmid >= g.k1) return;
   // ---- phase B (two-phase consumer): the group's remote parts ------------
   // after its sources' READY; only rows with remote nonzeros are updated
   // (read-modify-write of rows this unit itself just wrote, in L2)
-  if (!unit_wait<WAIT>(a, u, target, li, LPR, mask)) return;
+  if (STAGE == 1) {
+    if (!sources_ready(a, u, target, li, LPR, mask)) {
+      defer_unit(a, u, li);
+      return;
+    }
+  } else if (!unit_wait<(STAGE == 2 || WAIT)>(a, u, target, li, LPR, mask)) {
+    return;
+  }
   int rcur = -1;
   auto flush_b = [&]() {
     int64_t orow;
@@ -429,50 +476,79 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
   if (rcur >= 0) flush_b();
 }
 
+// Last warp of a consumer launch: the step-end barrier (READY from every
+// peer, also those this rank reads nothing from), then re-arm the counters
+// and advance the epoch the next step waits for.
+__device__ __forceinline__ void consumer_epilogue(const SpmmArgs &a, int32_t target, int lane,
+                                                  int nwarps) {
+  __syncwarp();
+  int last = 0;
+  if (lane == 0) {
+    __threadfence();
+    last = atomicAdd(a.done_ctr, 1) == nwarps - 1;
+  }
+  if (__shfl_sync(0xffffffffu, last, 0)) {
+    const uint64_t all = a.wait_all >= 64 ? ~0ull : ((1ull << a.wait_all) - 1ull);
+    wait_sources(a.ready, all, target, a.wait_err, a.wait_timeout_ns, lane, 32, 0xffffffffu);
+    if (lane == 0) {
+      *a.done_ctr = 0;
+      if (a.defer_n) { *a.defer_n = 0; *a.work_ctr = 0; }
+      __threadfence();
+      *reinterpret_cast<volatile int32_t *>(a.wait_epoch) = target;
+    }
+  }
+}
+
 // N <= 128 (VPL = 1): one-warp CTAs (BS = 32), 32 resident per SM; wider
 // rows (VPL > 1) keep 8-warp CTAs without a residency floor (no spills).
+// WAIT: remote SpMM with per-unit source waits (launched after this GPU's
+// producer and READY).  PH + STAGE 1: the two-phase consumer's first launch
+// (concurrent with the producer, never spins); PH + STAGE 2: its deferred
+// continuation (after this GPU's producer and READY; a persistent grid pulls
+// the deferred units).
 template <int LPR, int VPL, bool ACCUM, bool TWO, int U, bool OUTP, int HINT, bool WAIT,
-          int BS = 32, int MINB = 32, bool PF = false, bool PH = false>
+          int BS = 32, int MINB = 32, bool PF = false, bool PH = false, int STAGE = 0>
 __global__ void __launch_bounds__(BS, MINB) k_spmm(const SpmmArgs a) {
   constexpr int R = 32 / LPR;   // lane groups per warp
+  constexpr int UU = (U < LPR ? U : LPR);
   const int lane = threadIdx.x & 31;
   const int sub = lane / LPR;
   const int li = lane % LPR;
   const unsigned mask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (sub * LPR));
   const int64_t u = (((int64_t)blockIdx.x * BS + threadIdx.x) >> 5) * R + sub;
+  if (PH && STAGE == 1) {
+    const int32_t target = *reinterpret_cast<volatile int32_t *>(a.wait_epoch) + 1;
+    spmm_unit<LPR, VPL, ACCUM, TWO, UU, OUTP, HINT, true, false, true, false, 1>(a, u, li, mask,
+                                                                                target);
+    return;
+  }
+  if (PH && STAGE == 2) {
+    const int32_t target = *reinterpret_cast<volatile int32_t *>(a.wait_epoch) + 1;
+    const int32_t nd = *reinterpret_cast<volatile int32_t *>(a.defer_n);
+    for (;;) {
+      int i = 0;
+      if (li == 0) i = atomicAdd(a.work_ctr, 1);
+      i = __shfl_sync(mask, i, 0, LPR);
+      if (i >= nd) break;
+      spmm_unit<LPR, VPL, ACCUM, TWO, UU, OUTP, HINT, true, false, true, true, 2>(
+          a, a.defer_list[i], li, mask, target);
+    }
+    consumer_epilogue(a, target, lane, (int)(gridDim.x * (BS / 32)));
+    return;
+  }
   if (WAIT) {
     // target epoch read before this warp is counted done (the last warp
     // advances it, after every warp has read it)
     const int32_t target = *reinterpret_cast<volatile int32_t *>(a.wait_epoch) + 1;
-    if (PH) {   // two-phase consumer: waits between its local and remote parts
-      spmm_unit<LPR, VPL, ACCUM, TWO, (U < LPR ? U : LPR), OUTP, HINT, true, false, true, true>(
-          a, u, li, mask, target);
-    } else {    // remote SpMM: each lane group waits for its own unit's sources first
-      const bool in = u < (int64_t)a.n_tasks + a.n_groups;
-      if (in && unit_wait<true>(a, u, target, li, LPR, mask))
-        spmm_unit<LPR, VPL, ACCUM, TWO, (U < LPR ? U : LPR), OUTP, HINT, true>(a, u, li, mask);
-    }
-    __syncwarp();
-    int last = 0;
-    if (lane == 0) {
-      __threadfence();
-      last = atomicAdd(a.done_ctr, 1) == (int)(gridDim.x * (BS / 32)) - 1;
-    }
-    if (__shfl_sync(0xffffffffu, last, 0)) {
-      // step-end barrier: READY from every peer, also those this rank reads nothing from
-      const uint64_t all = a.wait_all >= 64 ? ~0ull : ((1ull << a.wait_all) - 1ull);
-      wait_sources(a.ready, all, target, a.wait_err, a.wait_timeout_ns, lane, 32, 0xffffffffu);
-      if (lane == 0) {
-        *a.done_ctr = 0;
-        __threadfence();
-        *reinterpret_cast<volatile int32_t *>(a.wait_epoch) = target;
-      }
-    }
+    // remote SpMM: each lane group waits for its own unit's sources first
+    const bool in = u < (int64_t)a.n_tasks + a.n_groups;
+    if (in && unit_wait<true>(a, u, target, li, LPR, mask))
+      spmm_unit<LPR, VPL, ACCUM, TWO, UU, OUTP, HINT, true>(a, u, li, mask);
+    consumer_epilogue(a, target, lane, (int)(gridDim.x * (BS / 32)));
     return;
   }
   // two-phase without waits (loopback): coherent loads of the second source
-  spmm_unit<LPR, VPL, ACCUM, TWO, (U < LPR ? U : LPR), OUTP, HINT, PH, PF, PH, false>(a, u, li,
-                                                                                      mask);
+  spmm_unit<LPR, VPL, ACCUM, TWO, UU, OUTP, HINT, PH, PF, PH, false>(a, u, li, mask);
 }
 
 // Generic width (N not a supported vector width): one warp per CSR row,
@@ -675,8 +751,17 @@ void spmm_launch(const SpmmArgs &a, bool acc, cudaStream_t s) {
   const int64_t per_cta = (int64_t)(BS / 32) * (32 / LPR);
   const unsigned grid = (unsigned)((units + per_cta - 1) / per_cta);
   const bool two = a.X1 != nullptr;
-  if (a.ready && a.long_mid) {   // two-phase consumer (CX): waits between its phases
-    k_spmm<LPR, VPL, false, true, U, false, 0, true, BS, MINB, false, true><<<grid, BS, 0, s>>>(a);
+  if (a.ready && a.long_mid) {   // two-phase consumer (CX): stage 1 or its deferred stage 2
+    if (a.cx_stage == 1) {
+      k_spmm<LPR, VPL, false, true, U, false, 0, false, BS, MINB, false, true, 1>
+          <<<grid, BS, 0, s>>>(a);
+    } else {
+      const int64_t per_cta2 = (int64_t)(BS / 32) * (32 / LPR);
+      const int64_t cap = ((int64_t)num_sms() * 32 * 32 / BS) ;   // one wave of lane groups
+      const unsigned g2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>((units + per_cta2 - 1) / per_cta2, cap));
+      k_spmm<LPR, VPL, false, true, U, false, 0, false, BS, MINB, false, true, 2>
+          <<<g2, BS, 0, s>>>(a);
+    }
   } else if (a.ready) {   // remote SpMM with per-unit source waits, coherent loads
     k_spmm<LPR, VPL, true, false, U, false, 0, true, BS, MINB, false, false><<<grid, BS, 0, s>>>(a);
   } else if (a.long_mid) {   // two-phase consumer without waits (loopback)

@@ -77,6 +77,14 @@ struct SpmmArgs {
   int32_t *wait_err = nullptr;
   int32_t *done_ctr = nullptr;          // zero-initialised
   int32_t wait_all = 0;                 // P (the last warp's barrier)
+  // two-phase consumer: launch stage (1 = concurrent first launch that defers
+  // units whose sources are not READY yet, 2 = their continuation), the
+  // deferred-unit list [n_tasks + n_groups], its length and a work counter
+  // (all zero-initialised; re-armed by stage 2's last warp)
+  int32_t cx_stage = 0;
+  int32_t *defer_list = nullptr;
+  int32_t *defer_n = nullptr;
+  int32_t *work_ctr = nullptr;
   int64_t wait_timeout_ns = 0;
 };
 

@@ -517,6 +517,9 @@ void upload_merged(Plan &pl) {
     throw Error(SHIRO_E_ARG, "two-phase consumer: more than 2^31 source rows");
   Arena ar2;
   SpmmLayout L = layout_spmm(ar2, cx, pl.N);
+  const size_t units = L.sp.task_long.size() + L.sp.groups.size();
+  const size_t o_def = ar2.reserve(std::max<size_t>(1, units) * sizeof(int32_t));   // deferred list
+  const size_t o_ctr = ar2.reserve(2 * sizeof(int32_t));                            // defer_n, work_ctr
   if (pl.merged_ops) cudaFree(pl.merged_ops);
   SHIRO_CK(cudaMalloc(&pl.merged_ops, std::max<size_t>(ar2.total, 256)));
   SHIRO_CK(cudaMemset(pl.merged_ops, 0, std::max<size_t>(ar2.total, 256)));
@@ -525,6 +528,9 @@ void upload_merged(Plan &pl) {
     if (it.src && it.bytes)
       SHIRO_CK(cudaMemcpy(base + it.off, it.src, it.bytes, cudaMemcpyHostToDevice));
   pl.d_cx = bind_spmm(base, L, cx, pl.N);
+  pl.d_cx.a.defer_list = reinterpret_cast<int32_t *>(base + o_def);
+  pl.d_cx.a.defer_n = reinterpret_cast<int32_t *>(base + o_ctr);
+  pl.d_cx.a.work_ctr = reinterpret_cast<int32_t *>(base + o_ctr) + 1;
   pl.refresh_ops.push_back(&pl.d_cx);
   pl.info.dev_bytes += (int64_t)ar2.total;
   // the consumer carries the local (K1) and remote (K2 + K5) work of a step
@@ -847,8 +853,10 @@ void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
   const int par = pl.dbuf ? pl.step_parity : 0;
   float *rb = par ? pl.recv_buf2 : pl.recv_buf;
   if (pl.merged) {
-    // two-phase consumer: producer (s_hi) || CX (s: K1 parts, then per-source
-    // waits, then K2 + K5 parts)
+    // two-phase consumer: producer (s_hi) || CX stage 1 (s: every unit's K1
+    // part, its K2 + K5 part too if its sources are READY already, else the
+    // unit is deferred); after this GPU's producer + READY: CX stage 2 (the
+    // deferred units, with per-source waits) -- no warp spins before the join
     rec(0, s);
     SHIRO_CK(cudaEventRecord(pl.ev_fork, s));
     SHIRO_CK(cudaStreamWaitEvent(pl.s_hi, pl.ev_fork, 0));
@@ -869,14 +877,20 @@ void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
       cx.a.done_ctr = done;
       cx.a.wait_all = P;
       cx.a.wait_timeout_ns = pl.wait_timeout_ns;
+      cx.a.cx_stage = 1;
+      launches += run_spmm(cx, B, pl.M, rb, C, false, s);
+      rec(3, s);
+      SHIRO_CK(cudaStreamWaitEvent(s, pl.ev_join, 0));
+      cx.a.cx_stage = 2;
       launches += run_spmm(cx, B, pl.M, rb, C, false, s);
     } else {   // no local rows: the step-end barrier alone
+      rec(3, s);
+      SHIRO_CK(cudaStreamWaitEvent(s, pl.ev_join, 0));
       launches += launch_wait(pl.xflags, P, ep_wait, 1, err, pl.wait_timeout_ns, s, true);
     }
-    rec(3, s);
-    SHIRO_CK(cudaStreamWaitEvent(s, pl.ev_join, 0));
-    if (!pl.dbuf) launches += launch_signal(pl.consumed_ptrs, P - 1, ep_wait, 0, false, s);
     rec(4, s);
+    if (!pl.dbuf) launches += launch_signal(pl.consumed_ptrs, P - 1, ep_wait, 0, false, s);
+    rec(5, s);
     SHIRO_CK(cudaMemcpyAsync(pl.err_host, err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     pl.last_launches = launches;
     pl.prof_used = 5;
@@ -1785,14 +1799,15 @@ int shiro_stage_times(shiro_plan_t plan, double *ms) {
       return;
     }
     if (pl.prof_used == 5) {
-      // two-phase consumer (default fused exchange): PARTIAL = producer (K4
-      // + K3 -> peers), EXCHANGE = its READY signal, REMOTE = the consumer
-      // launch (K1 + K2 + K5 with its per-source waits), from the step's
-      // start (the branches overlap); LOCAL is not separable (0)
+      // two-phase consumer (SHIRO_CX=1): PARTIAL = producer (K4 + K3 ->
+      // peers), EXCHANGE = its READY signal, LOCAL = CX stage 1 (every K1
+      // part plus the K2 + K5 parts already READY; concurrent with the
+      // producer, from the step's start), REMOTE = stage 2 (deferred units)
       ms[SHIRO_STAGE_PARTIAL] = el(0, 1);
       ms[SHIRO_STAGE_EXCHANGE] = el(1, 2);
-      ms[SHIRO_STAGE_REMOTE] = el(0, 3);
-      ms[SHIRO_STAGE_TOTAL] = el(0, 4);
+      ms[SHIRO_STAGE_LOCAL] = el(0, 3);
+      ms[SHIRO_STAGE_REMOTE] = el(3, 4);
+      ms[SHIRO_STAGE_TOTAL] = el(0, 5);
       return;
     }
     if (pl.prof_used == 3) {

@@ -30,7 +30,8 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, flags, g, cfg_name, out_q):
+def _worker(rank, world, port, flags, g, cfg_name, env, out_q):
+    os.environ.update(env)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     os.environ.setdefault("SHIRO_P2P_TIMEOUT_MS", "60000")
@@ -81,11 +82,11 @@ def _worker(rank, world, port, flags, g, cfg_name, out_q):
         dist.destroy_process_group()
 
 
-def _run(world, flags, g=1, cfg="c2"):
+def _run(world, flags, g=1, cfg="c2", env=None):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, flags, g, cfg, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, flags, g, cfg, env or {}, q))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -98,15 +99,19 @@ def _run(world, flags, g=1, cfg="c2"):
         assert bad == 0, (rank, bad)
 
 
-@pytest.mark.parametrize("flags", ["fused", "nccl", "nccl-split"])
+@pytest.mark.parametrize("flags", ["fused", "fused-two-phase", "fused-k_wait", "nccl",
+                                   "nccl-split"])
 def test_two_gpus_exchanges_exact(flags):
     import paper_2512_20178_b200 as sh
-    f = {"fused": 0, "nccl": sh.F_XCHG_NCCL, "nccl-split": sh.F_XCHG_NCCL | sh.F_SPLIT_RECV}[flags]
-    _run(2, f)
+    f = {"nccl": sh.F_XCHG_NCCL, "nccl-split": sh.F_XCHG_NCCL | sh.F_SPLIT_RECV}.get(flags, 0)
+    env = {"fused-two-phase": {"SHIRO_CX": "1", "SHIRO_P2P_TIMEOUT_MS": "20000"},
+           "fused-k_wait": {"SHIRO_INKERNEL_WAIT": "0"}}.get(flags, {})
+    _run(2, f, env=env)
 
 
 def test_four_gpus_flat_and_hierarchical_exact():
     if torch.cuda.device_count() < 4:
         pytest.skip("needs 4 GPUs")
     _run(4, 0)
+    _run(4, 0, env={"SHIRO_CX": "1", "SHIRO_P2P_TIMEOUT_MS": "20000"})
     _run(4, 0, g=2)
