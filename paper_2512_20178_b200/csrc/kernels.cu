@@ -65,15 +65,19 @@ __device__ __forceinline__ int2 ldcv_h(const int2 *p) {
   return v;
 }
 // gathered source row: HINT 0 plain LDG; 2 evict_last; 3 evict_last for hot
-// rows, evict_first otherwise; COH (and coh for this row): ld.global.cg
-// (coherent at L2: rows that peers store during the launch)
+// rows, evict_first otherwise; COH (and coh for this row): a weak
+// (coherent-path, L1-cacheable) load instead of the read-only ld.global.nc:
+// peers store into other parts of the buffer during the launch, and these
+// rows are only read after this lane group's ld.acquire.sys of their READY
+// flag (memory-model ordered, unlike the non-coherent path)
 template <int HINT, bool COH>
 __device__ __forceinline__ float4 ldB(const float4 *p, bool hot, bool coh) {
   float4 v;
   if (COH && coh) {
-    asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];"
+    asm volatile("ld.global.v4.f32 {%0, %1, %2, %3}, [%4];"
                  : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                 : "l"(p));
+                 : "l"(p)
+                 : "memory");
   } else if (HINT == 0) {
     v = __ldg(p);
   } else if (HINT == 2 || hot) {
@@ -476,29 +480,6 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
   if (rcur >= 0) flush_b();
 }
 
-// Last warp of a consumer launch: the step-end barrier (READY from every
-// peer, also those this rank reads nothing from), then re-arm the counters
-// and advance the epoch the next step waits for.
-__device__ __forceinline__ void consumer_epilogue(const SpmmArgs &a, int32_t target, int lane,
-                                                  int nwarps) {
-  __syncwarp();
-  int last = 0;
-  if (lane == 0) {
-    __threadfence();
-    last = atomicAdd(a.done_ctr, 1) == nwarps - 1;
-  }
-  if (__shfl_sync(0xffffffffu, last, 0)) {
-    const uint64_t all = a.wait_all >= 64 ? ~0ull : ((1ull << a.wait_all) - 1ull);
-    wait_sources(a.ready, all, target, a.wait_err, a.wait_timeout_ns, lane, 32, 0xffffffffu);
-    if (lane == 0) {
-      *a.done_ctr = 0;
-      if (a.defer_n) { *a.defer_n = 0; *a.work_ctr = 0; }
-      __threadfence();
-      *reinterpret_cast<volatile int32_t *>(a.wait_epoch) = target;
-    }
-  }
-}
-
 // N <= 128 (VPL = 1): one-warp CTAs (BS = 32), 32 resident per SM; wider
 // rows (VPL > 1) keep 8-warp CTAs without a residency floor (no spills).
 // WAIT: remote SpMM with per-unit source waits (launched after this GPU's
@@ -533,8 +514,7 @@ __global__ void __launch_bounds__(BS, MINB) k_spmm(const SpmmArgs a) {
       spmm_unit<LPR, VPL, ACCUM, TWO, UU, OUTP, HINT, true, false, true, true, 2>(
           a, a.defer_list[i], li, mask, target);
     }
-    consumer_epilogue(a, target, lane, (int)(gridDim.x * (BS / 32)));
-    return;
+    return;   // the step-end barrier and the epoch advance are the next launch (k_wait)
   }
   if (WAIT) {
     // target epoch read before this warp is counted done (the last warp
@@ -544,8 +524,7 @@ __global__ void __launch_bounds__(BS, MINB) k_spmm(const SpmmArgs a) {
     const bool in = u < (int64_t)a.n_tasks + a.n_groups;
     if (in && unit_wait<true>(a, u, target, li, LPR, mask))
       spmm_unit<LPR, VPL, ACCUM, TWO, UU, OUTP, HINT, true>(a, u, li, mask);
-    consumer_epilogue(a, target, lane, (int)(gridDim.x * (BS / 32)));
-    return;
+    return;   // the step-end barrier and the epoch advance are the next launch (k_wait)
   }
   // two-phase without waits (loopback): coherent loads of the second source
   spmm_unit<LPR, VPL, ACCUM, TWO, UU, OUTP, HINT, PH, PF, PH, false>(a, u, li, mask);

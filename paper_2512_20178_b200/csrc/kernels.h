@@ -66,21 +66,19 @@ struct SpmmArgs {
   // L2-coherent loads (the buffer is written by peers during the launch).
   // A timeout (per warp, %globaltimer) or an error raised by any other warp
   // sets / sees *wait_err and skips the unit instead of hanging the GPU.
-  // The last warp to finish first waits for EVERY source 0..wait_all-1 (the
-  // step-end barrier of the double-buffered exchange), then advances
-  // *wait_epoch (done_ctr re-armed).  ready == nullptr: off.  With ready the
+  // *wait_epoch is only read (target = *wait_epoch + 1); the step-end barrier
+  // (READY from every peer) and the epoch advance are the following k_wait
+  // launch.  ready == nullptr: off.  With ready the
   // launch must be a two-phase overwrite with two sources [X0 = B_local ||
   // X1 = receive buffer]; only X1 rows use coherent loads.
   const int32_t *ready = nullptr;       // [P] local READY flags (one per source)
   const uint64_t *unit_src = nullptr;   // [n_tasks + n_groups] source masks
   int32_t *wait_epoch = nullptr;
   int32_t *wait_err = nullptr;
-  int32_t *done_ctr = nullptr;          // zero-initialised
-  int32_t wait_all = 0;                 // P (the last warp's barrier)
   // two-phase consumer: launch stage (1 = concurrent first launch that defers
   // units whose sources are not READY yet, 2 = their continuation), the
   // deferred-unit list [n_tasks + n_groups], its length and a work counter
-  // (all zero-initialised; re-armed by stage 2's last warp)
+  // (all zero-initialised; re-armed by a memset after stage 2)
   int32_t cx_stage = 0;
   int32_t *defer_list = nullptr;
   int32_t *defer_n = nullptr;

@@ -848,7 +848,7 @@ void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
     if (pl.prof_on) SHIRO_CK(cudaEventRecord(pl.prof[i], st));
   };
   const int P = pl.P;
-  int32_t *err = pl.xflags + 2 * P, *ep_sig = err + 1, *ep_wait = err + 2, *done = err + 3;
+  int32_t *err = pl.xflags + 2 * P, *ep_sig = err + 1, *ep_wait = err + 2;
   int64_t launches = 0;
   const int par = pl.dbuf ? pl.step_parity : 0;
   float *rb = par ? pl.recv_buf2 : pl.recv_buf;
@@ -874,8 +874,6 @@ void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
       cx.a.ready = pl.xflags;
       cx.a.wait_epoch = ep_wait;
       cx.a.wait_err = err;
-      cx.a.done_ctr = done;
-      cx.a.wait_all = P;
       cx.a.wait_timeout_ns = pl.wait_timeout_ns;
       cx.a.cx_stage = 1;
       launches += run_spmm(cx, B, pl.M, rb, C, false, s);
@@ -883,11 +881,13 @@ void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
       SHIRO_CK(cudaStreamWaitEvent(s, pl.ev_join, 0));
       cx.a.cx_stage = 2;
       launches += run_spmm(cx, B, pl.M, rb, C, false, s);
-    } else {   // no local rows: the step-end barrier alone
+      SHIRO_CK(cudaMemsetAsync(pl.d_cx.a.defer_n, 0, 2 * sizeof(int32_t), s));   // re-arm
+    } else {
       rec(3, s);
       SHIRO_CK(cudaStreamWaitEvent(s, pl.ev_join, 0));
-      launches += launch_wait(pl.xflags, P, ep_wait, 1, err, pl.wait_timeout_ns, s, true);
     }
+    // step-end barrier (READY from every peer) and the epoch advance
+    launches += launch_wait(pl.xflags, P, ep_wait, 1, err, pl.wait_timeout_ns, s, true);
     rec(4, s);
     if (!pl.dbuf) launches += launch_signal(pl.consumed_ptrs, P - 1, ep_wait, 0, false, s);
     rec(5, s);
@@ -924,10 +924,10 @@ void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
     rem.a.ready = pl.xflags;
     rem.a.wait_epoch = ep_wait;
     rem.a.wait_err = err;
-    rem.a.done_ctr = done;
-    rem.a.wait_all = P;
     rem.a.wait_timeout_ns = pl.wait_timeout_ns;
     launches += run_spmm(rem, rb, pl.recv_rows, nullptr, C, true, s);
+    // step-end barrier (READY from every peer) and the epoch advance
+    launches += launch_wait(pl.xflags, P, ep_wait, 1, err, pl.wait_timeout_ns, s, true);
   } else {
     launches += launch_wait(pl.xflags, P, ep_wait, 1, err, pl.wait_timeout_ns, s, true);
     if (!split) {
