@@ -421,14 +421,14 @@ void upload_prod(Plan &pl, const std::vector<int32_t> &pack_src,
   const int64_t np = (int64_t)pack_src.size();
   const bool refresh = !pl.A_out.vsrc.empty() || !pl.A_diag.vsrc.empty();
   if (prod_ops_exist(pl)) { cudaFree(pl.prod_ops); pl.prod_ops = nullptr; }
-  for (int64_t i = 0; i < np; ++i) {
+  auto pack_row = [&](int64_t i) {
     c.col.push_back(pack_src[i]);
     c.val.push_back(1.0f);
     if (refresh) c.vsrc.push_back(-1);
     c.rp.push_back((int64_t)c.col.size());
     outp.push_back(pack_addr[i]);
     if (two) outp2.push_back((*pack_addr2)[i]);
-  }
+  };
   auto append = [&](const HostCsr &a, int64_t t) {
     for (int64_t k = a.rp[t]; k < a.rp[t + 1]; ++k) {
       c.col.push_back(a.col[k]);
@@ -437,10 +437,33 @@ void upload_prod(Plan &pl, const std::vector<int32_t> &pack_src,
     }
     c.rp.push_back((int64_t)c.col.size());
   };
-  for (int64_t t = 0; t < pl.A_out.nrows; ++t) {
+  auto part_row = [&](int64_t t) {
     append(pl.A_out, t);
     outp.push_back(part_addr[t]);
     if (two) outp2.push_back((*part_addr2)[t]);
+  };
+  // Flat exchange: the rows for peer d are the send_b[d] pack rows and the
+  // send_c[d] partial rows (both lists peer-ascending).  Every rank visits
+  // its peers in its own rotated order rank+1, rank+2, ... so that at any
+  // moment the P producers store into P different receivers instead of all
+  // into the same one (incast on one GPU's NVLink ports); the destinations
+  // are per-row addresses, so the order is free.
+  int64_t nb = 0, nc = 0;
+  for (int d = 0; d < pl.P; ++d) { nb += (int64_t)pl.send_b[d].size(); nc += (int64_t)pl.send_c[d].size(); }
+  if (!with_local && nb == np && nc == pl.A_out.nrows && pl.P > 1) {
+    std::vector<int64_t> b0(pl.P + 1, 0), c0(pl.P + 1, 0);
+    for (int d = 0; d < pl.P; ++d) {
+      b0[d + 1] = b0[d] + (int64_t)pl.send_b[d].size();
+      c0[d + 1] = c0[d] + (int64_t)pl.send_c[d].size();
+    }
+    for (int k = 1; k < pl.P; ++k) {
+      const int d = (pl.rank + k) % pl.P;
+      for (int64_t i = b0[d]; i < b0[d + 1]; ++i) pack_row(i);
+      for (int64_t t = c0[d]; t < c0[d + 1]; ++t) part_row(t);
+    }
+  } else {
+    for (int64_t i = 0; i < np; ++i) pack_row(i);
+    for (int64_t t = 0; t < pl.A_out.nrows; ++t) part_row(t);
   }
   if (with_local)
     for (int64_t t = 0; t < pl.A_diag.nrows; ++t) {
