@@ -22,7 +22,7 @@ import shiro_gen  # noqa: E402
 
 def main():
     names = sys.argv[1:] or ["c1", "c2", "c3", "c4"]
-    path = os.path.join(ROOT, "profiles", "bytes_table.json")
+    path = os.environ.get("BYTES_TABLE_OUT", os.path.join(ROOT, "profiles", "bytes_table.json"))
     table = json.load(open(path)) if os.path.exists(path) else {}
     for name in names:
         c = shiro_gen.CONFIGS[name]
