@@ -842,14 +842,17 @@ void exec_hier(Plan &pl, const float *B, float *C, cudaStream_t s) {
 // producer from being scheduled.  Epochs: ep_sig (advanced by the READY
 // signal) and ep_wait (advanced by the remote SpMM's last warp) live in
 // device memory, so the whole step is one replayable CUDA graph.
-// SHIRO_INKERNEL_WAIT=0: the consumer waits for all peers in a k_wait launch.
+// Consumer wait of the fused exchange.  Default: one k_wait launch for every
+// peer's READY, then the remote SpMM with read-only (L1-cached) loads.
+// SHIRO_INKERNEL_WAIT=1: per-source consumption -- every remote work unit
+// waits (in the kernel) only for the READY of the sources it reads.  Measured
+// on 2 and 4 B200 (profiles/r2m4b_*, r2m2e_*): on one NVSwitch box the peers'
+// rows land within microseconds of each other (balanced producers, rotated
+// peer order), so the per-unit acquires cost more than they overlap (c2/P=4
+// 0.0695 vs 0.0654 ms, c3 1.214 vs 1.184, c4 0.802 vs 0.798).
 bool inkernel_wait_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char *e = getenv("SHIRO_INKERNEL_WAIT");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
+  const char *e = getenv("SHIRO_INKERNEL_WAIT");   // read per step (cheap)
+  return e && e[0] == '1';
 }
 
 // The split consumer is used with the in-kernel waits, the fused K2+K5 and a

@@ -99,13 +99,14 @@ def _run(world, flags, g=1, cfg="c2", env=None):
         assert bad == 0, (rank, bad)
 
 
-@pytest.mark.parametrize("flags", ["fused", "fused-two-phase", "fused-k_wait", "nccl",
+@pytest.mark.parametrize("flags", ["fused", "fused-two-phase", "fused-per-unit-waits", "nccl",
                                    "nccl-split"])
 def test_two_gpus_exchanges_exact(flags):
     import paper_2512_20178_b200 as sh
     f = {"nccl": sh.F_XCHG_NCCL, "nccl-split": sh.F_XCHG_NCCL | sh.F_SPLIT_RECV}.get(flags, 0)
-    env = {"fused-two-phase": {"SHIRO_CX": "1", "SHIRO_P2P_TIMEOUT_MS": "20000"},
-           "fused-k_wait": {"SHIRO_INKERNEL_WAIT": "0"}}.get(flags, {})
+    env = {"fused-two-phase": {"SHIRO_INKERNEL_WAIT": "1", "SHIRO_CX": "1",
+                               "SHIRO_P2P_TIMEOUT_MS": "20000"},
+           "fused-per-unit-waits": {"SHIRO_INKERNEL_WAIT": "1"}}.get(flags, {})
     _run(2, f, env=env)
 
 
@@ -113,5 +114,6 @@ def test_four_gpus_flat_and_hierarchical_exact():
     if torch.cuda.device_count() < 4:
         pytest.skip("needs 4 GPUs")
     _run(4, 0)
-    _run(4, 0, env={"SHIRO_CX": "1", "SHIRO_P2P_TIMEOUT_MS": "20000"})
+    _run(4, 0, env={"SHIRO_INKERNEL_WAIT": "1"})
+    _run(4, 0, env={"SHIRO_INKERNEL_WAIT": "1", "SHIRO_CX": "1", "SHIRO_P2P_TIMEOUT_MS": "20000"})
     _run(4, 0, g=2)

@@ -157,10 +157,13 @@ def _check(res):
         assert bad == 0, (rank, bad)
 
 
-@pytest.mark.parametrize("env", [{}, {"SHIRO_DBUF": "0"}, {"SHIRO_INKERNEL_WAIT": "0"},
-                                 {"SHIRO_CX": "1"}, {"SHIRO_CX": "1", "SHIRO_DBUF": "0"}],
-                         ids=["default", "single-buffer", "separate-wait-launch",
-                              "two-phase-consumer", "two-phase-single-buffer"])
+@pytest.mark.parametrize("env", [{}, {"SHIRO_DBUF": "0"}, {"SHIRO_INKERNEL_WAIT": "1"},
+                                 {"SHIRO_INKERNEL_WAIT": "1", "SHIRO_DBUF": "0"},
+                                 {"SHIRO_INKERNEL_WAIT": "1", "SHIRO_CX": "1"},
+                                 {"SHIRO_INKERNEL_WAIT": "1", "SHIRO_CX": "1", "SHIRO_DBUF": "0"}],
+                         ids=["default", "single-buffer", "per-unit-waits",
+                              "per-unit-waits-single-buffer", "two-phase-consumer",
+                              "two-phase-single-buffer"])
 def test_two_process_fused_exchange_exact(env):
     import paper_2512_20178_b200 as sh
     for flags in (0, sh.F_SPLIT_RECV):

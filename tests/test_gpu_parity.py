@@ -133,6 +133,7 @@ def test_loopback_two_phase_consumer_exact(P, N, monkeypatch):
     per row group [local parts || remote parts], hub rows split at the local
     / remote boundary; integer data exact."""
     monkeypatch.setenv("SHIRO_CX", "1")
+    monkeypatch.setenv("SHIRO_INKERNEL_WAIT", "1")
     rng = np.random.default_rng(P * 7 + N)
     n = 2500
     row_ptr, col = hub_matrix(rng, n, 2000, 0.004)
