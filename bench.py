@@ -173,6 +173,25 @@ def nvlink_bytes(gpu_index):
                 tx += v[0].value.ullVal
                 rx += v[1].value.ullVal
                 got = True
+        if got:
+            return (tx * 1024, rx * 1024)
+    except Exception:
+        pass
+    # fallback: `nvidia-smi nvlink -gt d` (per-link "Tx"/"Rx" data counters, KiB)
+    try:
+        out = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", str(gpu_index)],
+                             capture_output=True, text=True, timeout=20).stdout
+        import re
+        tx = rx = 0
+        got = False
+        for line in out.splitlines():
+            m = re.search(r"(Tx|Rx)[^0-9]*([0-9]+)", line)
+            if m:
+                got = True
+                if m.group(1) == "Tx":
+                    tx += int(m.group(2))
+                else:
+                    rx += int(m.group(2))
         return (tx * 1024, rx * 1024) if got else None
     except Exception:
         return None
