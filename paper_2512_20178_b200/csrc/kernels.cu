@@ -64,42 +64,103 @@ __device__ __forceinline__ int2 ldcv_h(const int2 *p) {
   }
   return v;
 }
+// Per-lane vector of the SpMM: W floats (float, float2, float4).  N = 32 and
+// 64 run one 32-lane group per warp with float / float2 lanes (no divergent
+// lane groups inside a warp); N = 128 float4; N = 256 / 512 several float4.
+template <int W> struct VT;
+template <> struct VT<1> {
+  using T = float;
+  static __device__ __forceinline__ T zero() { return 0.f; }
+};
+template <> struct VT<2> {
+  using T = float2;
+  static __device__ __forceinline__ T zero() { return make_float2(0.f, 0.f); }
+};
+template <> struct VT<4> {
+  using T = float4;
+  static __device__ __forceinline__ T zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+};
+
+__device__ __forceinline__ void fma4(float &acc, float v, const float &x) { acc = fmaf(v, x, acc); }
+__device__ __forceinline__ void fma4(float2 &acc, float v, const float2 &x) {
+  acc.x = fmaf(v, x.x, acc.x);
+  acc.y = fmaf(v, x.y, acc.y);
+}
+__device__ __forceinline__ void add4(float &acc, const float &x) { acc += x; }
+__device__ __forceinline__ void add4(float2 &acc, const float2 &x) { acc.x += x.x; acc.y += x.y; }
+
+// raw loads / stores of one per-lane vector with an optional L2 policy
+__device__ __forceinline__ float ld_weak(const float *p) {
+  float v;
+  asm volatile("ld.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ float2 ld_weak(const float2 *p) {
+  float2 v;
+  asm volatile("ld.global.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ float4 ld_weak(const float4 *p) {
+  float4 v;
+  asm volatile("ld.global.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ float ld_pol(const float *p, uint64_t pol) {
+  float v;
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float2 ld_pol(const float2 *p, uint64_t pol) {
+  float2 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;"
+               : "=f"(v.x), "=f"(v.y)
+               : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float4 ld_pol(const float4 *p, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_pol(float *p, const float &v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_pol(float2 *p, const float2 &v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(p), "f"(v.x), "f"(v.y),
+               "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void st_pol(float4 *p, const float4 &v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
+               : "memory");
+}
+
 // gathered source row: HINT 0 plain LDG; 2 evict_last; 3 evict_last for hot
 // rows, evict_first otherwise; COH (and coh for this row): a weak
 // (coherent-path, L1-cacheable) load instead of the read-only ld.global.nc:
 // peers store into other parts of the buffer during the launch, and these
 // rows are only read after this lane group's ld.acquire.sys of their READY
 // flag (memory-model ordered, unlike the non-coherent path)
-template <int HINT, bool COH>
-__device__ __forceinline__ float4 ldB(const float4 *p, bool hot, bool coh) {
-  float4 v;
-  if (COH && coh) {
-    asm volatile("ld.global.v4.f32 {%0, %1, %2, %3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                 : "l"(p)
-                 : "memory");
-  } else if (HINT == 0) {
-    v = __ldg(p);
-  } else if (HINT == 2 || hot) {
-    // the policy operand lives in a uniform register: one load per constant
-    // policy (a per-row select would make the compiler waterfall over lanes);
-    // `hot` is uniform across the lane group, so this branch never diverges
-    asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                 : "l"(p), "l"(pol_last()));
-  } else {
-    asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                 : "l"(p), "l"(pol_first()));
-  }
-  return v;
+template <int HINT, bool COH, typename V>
+__device__ __forceinline__ V ldB(const V *p, bool hot, bool coh) {
+  if (COH && coh) return ld_weak(p);
+  if (HINT == 0) return __ldg(p);
+  // the policy operand lives in a uniform register: one load per constant
+  // policy (a per-row select would make the compiler waterfall over lanes);
+  // `hot` is uniform across the lane group, so this branch never diverges
+  if (HINT == 2 || hot) return ld_pol(p, pol_last());
+  return ld_pol(p, pol_first());
 }
-template <int HINT>
-__device__ __forceinline__ void stY_h(float4 *p, const float4 &v) {
+template <int HINT, typename V>
+__device__ __forceinline__ void stY_h(V *p, const V &v) {
   if (HINT == 0) { *p = v; return; }
-  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x),
-               "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol_first())
-               : "memory");
+  st_pol(p, v, pol_first());
 }
 
 __device__ __forceinline__ int ld_stream_u8(const uint8_t *p) {
@@ -125,9 +186,9 @@ __device__ __forceinline__ const float *src_row_ptr(const SpmmArgs &a, int c) {
   if (TWO && c >= a.n0) return a.X1 + (uint64_t)(uint32_t)(c - (int)a.n0) * (uint32_t)a.N;
   return a.X0 + (uint64_t)(uint32_t)c * (uint32_t)a.N;
 }
-template <bool TWO>
-__device__ __forceinline__ const float4 *src_row(const SpmmArgs &a, int c) {
-  return reinterpret_cast<const float4 *>(src_row_ptr<TWO>(a, c));
+template <bool TWO, typename V>
+__device__ __forceinline__ const V *src_row(const SpmmArgs &a, int c) {
+  return reinterpret_cast<const V *>(src_row_ptr<TWO>(a, c));
 }
 
 __device__ __forceinline__ uint64_t gtimer() {
@@ -181,16 +242,17 @@ __device__ __forceinline__ void prefetch_row(const SpmmArgs &a, int c) {
 // Output row address of a pointer-routed row: a peer (or own) buffer address,
 // or -- top bit set -- a row index into Y (the caller's C: local rows of the
 // hierarchical Stage-I launch, whose address is only known at call time).
-__device__ __forceinline__ float4 *out_addr(const SpmmArgs &a, long long v) {
-  if (v < 0) return reinterpret_cast<float4 *>(a.Y + (v & 0x7fffffffffffffffLL) * a.N);
-  return reinterpret_cast<float4 *>(v);
+template <typename V>
+__device__ __forceinline__ V *out_addr(const SpmmArgs &a, long long v) {
+  if (v < 0) return reinterpret_cast<V *>(a.Y + (v & 0x7fffffffffffffffLL) * a.N);
+  return reinterpret_cast<V *>(v);
 }
 
 
 // Gather U source rows for nonzeros j..j+U-1 of the current batch; the
 // weights are broadcast together with the columns, before any FMA.
-template <int LPR, int VPL, bool TWO, int U, int HINT, bool COH>
-__device__ __forceinline__ void gather(const SpmmArgs &a, float4 (&x)[U][VPL], float (&w)[U],
+template <int LPR, int VPL, int W, bool TWO, int U, int HINT, bool COH>
+__device__ __forceinline__ void gather(const SpmmArgs &a, typename VT<W>::T (&x)[U][VPL], float (&w)[U],
                                        int c, float v, int j, int cnt, int li, unsigned mask) {
 #pragma unroll
   for (int u = 0; u < U; ++u) {
@@ -198,7 +260,7 @@ __device__ __forceinline__ void gather(const SpmmArgs &a, float4 (&x)[U][VPL], f
     const float vu = __shfl_sync(mask, v, j + u, LPR);
     if (j + u < cnt) {               // uniform across the lane group
       // hot marks (bit 31) exist only in HINT 3 launches
-      const float4 *r = src_row<TWO>(a, HINT == 3 ? (cu & 0x7fffffff) : cu);
+      const typename VT<W>::T *r = src_row<TWO, typename VT<W>::T>(a, HINT == 3 ? (cu & 0x7fffffff) : cu);
       // with two sources only the second one (the receive buffer) is written
       // by peers during the launch
       const bool coh = !TWO || cu >= a.n0;
@@ -208,7 +270,7 @@ __device__ __forceinline__ void gather(const SpmmArgs &a, float4 (&x)[U][VPL], f
       w[u] = vu;
     } else {
 #pragma unroll
-      for (int q = 0; q < VPL; ++q) x[u][q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int q = 0; q < VPL; ++q) x[u][q] = VT<W>::zero();
       w[u] = 0.f;
     }
   }
@@ -252,13 +314,13 @@ __device__ __forceinline__ void defer_unit(const SpmmArgs &a, int64_t u, int li)
 // READY, else the unit is deferred (a hub chunk parks its partial in its
 // scratch row) -- never spins; 2 = the deferred continuation: phase B after
 // waiting for the sources (launched after this GPU's producer and READY).
-template <int LPR, int VPL, bool ACCUM, bool TWO, int U, bool OUTP, int HINT, bool COH,
+template <int LPR, int VPL, int W, bool ACCUM, bool TWO, int U, bool OUTP, int HINT, bool COH,
           bool PF = false, bool PH = false, bool WAIT = false, int STAGE = 0>
 __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, const int li,
                                           const unsigned mask, const int32_t target = 0) {
-  float4 acc[VPL];
+  typename VT<W>::T acc[VPL];
 #pragma unroll
-  for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int q = 0; q < VPL; ++q) acc[q] = VT<W>::zero();
 
   if (u < a.n_tasks) {
     // ---- chunk of a long (hub) row -------------------------------------
@@ -281,9 +343,9 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
         }
         const int cnt = (int)((k1 - base) < LPR ? (k1 - base) : LPR);
         for (int j = 0; j < cnt; j += U) {
-          float4 x[U][VPL];
+          typename VT<W>::T x[U][VPL];
           float w[U];
-          gather<LPR, VPL, TWO, U, HINT, COH>(a, x, w, cv.x, __int_as_float(cv.y), j, cnt, li, mask);
+          gather<LPR, VPL, W, TWO, U, HINT, COH>(a, x, w, cv.x, __int_as_float(cv.y), j, cnt, li, mask);
 #pragma unroll
           for (int uu = 0; uu < U; ++uu)
 #pragma unroll
@@ -291,7 +353,7 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
         }
       }
     };
-    float4 *sp = reinterpret_cast<float4 *>(a.scratch + u * (int64_t)a.N);
+    typename VT<W>::T *sp = reinterpret_cast<typename VT<W>::T *>(a.scratch + u * (int64_t)a.N);
     if (STAGE == 2) {       // deferred continuation: the parked phase-A partial
 #pragma unroll
       for (int q = 0; q < VPL; ++q) acc[q] = __ldcg(sp + li + q * LPR);
@@ -318,30 +380,30 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
     last = __shfl_sync(mask, last, 0, LPR);
     if (last) {
       __threadfence();
-      float4 s[VPL];
+      typename VT<W>::T s[VPL];
 #pragma unroll
-      for (int q = 0; q < VPL; ++q) s[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int q = 0; q < VPL; ++q) s[q] = VT<W>::zero();
       // fixed chunk order (deterministic); 8 partial loads in flight
       for (int c0 = 0; c0 < nch; c0 += 8) {
-        float4 pv[8][VPL];
+        typename VT<W>::T pv[8][VPL];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          const float4 *cp = reinterpret_cast<const float4 *>(a.scratch + (int64_t)(f + c0 + c) * a.N);
+          const typename VT<W>::T *cp = reinterpret_cast<const typename VT<W>::T *>(a.scratch + (int64_t)(f + c0 + c) * a.N);
 #pragma unroll
           for (int q = 0; q < VPL; ++q)
-            pv[c][q] = (c0 + c < nch) ? __ldcg(cp + li + q * LPR) : make_float4(0.f, 0.f, 0.f, 0.f);
+            pv[c][q] = (c0 + c < nch) ? __ldcg(cp + li + q * LPR) : VT<W>::zero();
         }
 #pragma unroll
         for (int c = 0; c < 8; ++c)
 #pragma unroll
           for (int q = 0; q < VPL; ++q) add4(s[q], pv[c][q]);
       }
-      float4 *y;
+      typename VT<W>::T *y;
       if (OUTP) {
-        y = out_addr(a, (long long)a.out_ptr[t]);
+        y = out_addr<typename VT<W>::T>(a, (long long)a.out_ptr[t]);
       } else {
         const int64_t orow = a.out_row ? a.out_row[t] : t;
-        y = reinterpret_cast<float4 *>(a.Y + orow * a.N);
+        y = reinterpret_cast<typename VT<W>::T *>(a.Y + orow * a.N);
       }
 #pragma unroll
       for (int q = 0; q < VPL; ++q) {
@@ -372,10 +434,10 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
   }
   int cur = 0;   // current row offset inside the group
   auto flush = [&]() {
-    float4 *y;
+    typename VT<W>::T *y;
     if (OUTP) {
       const long long sel = (cur < LPR) ? opw0 : opw1;
-      y = out_addr(a, __shfl_sync(mask, sel, cur & (LPR - 1), LPR));
+      y = out_addr<typename VT<W>::T>(a, __shfl_sync(mask, sel, cur & (LPR - 1), LPR));
     } else {
       int64_t orow;
       if (a.out_row) {
@@ -384,13 +446,13 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
       } else {
         orow = g.r0 + cur;
       }
-      y = reinterpret_cast<float4 *>(a.Y + orow * a.N);
+      y = reinterpret_cast<typename VT<W>::T *>(a.Y + orow * a.N);
     }
 #pragma unroll
     for (int q = 0; q < VPL; ++q) {
       if (ACCUM) add4(acc[q], y[li + q * LPR]);
       stY_h<HINT>(y + li + q * LPR, acc[q]);
-      acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      acc[q] = VT<W>::zero();
     }
     ++cur;
   };
@@ -405,9 +467,9 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
     }
     const int cnt = (int)((kend - base) < LPR ? (kend - base) : LPR);
     for (int j = 0; j < cnt; j += U) {
-      float4 x[U][VPL];
+      typename VT<W>::T x[U][VPL];
       float w[U];
-      gather<LPR, VPL, TWO, U, HINT, COH>(a, x, w, cv.x, __int_as_float(cv.y), j, cnt, li, mask);
+      gather<LPR, VPL, W, TWO, U, HINT, COH>(a, x, w, cv.x, __int_as_float(cv.y), j, cnt, li, mask);
 #pragma unroll
       for (int uu = 0; uu < U; ++uu) {
         const int rou = __shfl_sync(mask, ro, j + uu, LPR);
@@ -442,12 +504,12 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
     } else {
       orow = g.r0 + rcur;
     }
-    float4 *y = reinterpret_cast<float4 *>(a.Y + orow * a.N);
+    typename VT<W>::T *y = reinterpret_cast<typename VT<W>::T *>(a.Y + orow * a.N);
 #pragma unroll
     for (int q = 0; q < VPL; ++q) {
       add4(acc[q], __ldcg(y + li + q * LPR));
       y[li + q * LPR] = acc[q];
-      acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      acc[q] = VT<W>::zero();
     }
   };
   for (int64_t base = g.kmid; base < g.k1; base += LPR) {
@@ -460,9 +522,9 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
     }
     const int cnt = (int)((g.k1 - base) < LPR ? (g.k1 - base) : LPR);
     for (int j = 0; j < cnt; j += U) {
-      float4 x[U][VPL];
+      typename VT<W>::T x[U][VPL];
       float w[U];
-      gather<LPR, VPL, TWO, U, HINT, COH>(a, x, w, cv.x, __int_as_float(cv.y), j, cnt, li, mask);
+      gather<LPR, VPL, W, TWO, U, HINT, COH>(a, x, w, cv.x, __int_as_float(cv.y), j, cnt, li, mask);
 #pragma unroll
       for (int uu = 0; uu < U; ++uu) {
         const int rou = __shfl_sync(mask, ro, j + uu, LPR);
@@ -487,7 +549,7 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
 // (concurrent with the producer, never spins); PH + STAGE 2: its deferred
 // continuation (after this GPU's producer and READY; a persistent grid pulls
 // the deferred units).
-template <int LPR, int VPL, bool ACCUM, bool TWO, int U, bool OUTP, int HINT, bool WAIT,
+template <int LPR, int VPL, int W, bool ACCUM, bool TWO, int U, bool OUTP, int HINT, bool WAIT,
           int BS = 32, int MINB = 32, bool PF = false, bool PH = false, int STAGE = 0>
 __global__ void __launch_bounds__(BS, MINB) k_spmm(const SpmmArgs a) {
   constexpr int R = 32 / LPR;   // lane groups per warp
@@ -499,7 +561,7 @@ __global__ void __launch_bounds__(BS, MINB) k_spmm(const SpmmArgs a) {
   const int64_t u = (((int64_t)blockIdx.x * BS + threadIdx.x) >> 5) * R + sub;
   if (PH && STAGE == 1) {
     const int32_t target = *reinterpret_cast<volatile int32_t *>(a.wait_epoch) + 1;
-    spmm_unit<LPR, VPL, ACCUM, TWO, UU, OUTP, HINT, true, false, true, false, 1>(a, u, li, mask,
+    spmm_unit<LPR, VPL, W, ACCUM, TWO, UU, OUTP, HINT, true, false, true, false, 1>(a, u, li, mask,
                                                                                 target);
     return;
   }
@@ -511,7 +573,7 @@ __global__ void __launch_bounds__(BS, MINB) k_spmm(const SpmmArgs a) {
       if (li == 0) i = atomicAdd(a.work_ctr, 1);
       i = __shfl_sync(mask, i, 0, LPR);
       if (i >= nd) break;
-      spmm_unit<LPR, VPL, ACCUM, TWO, UU, OUTP, HINT, true, false, true, true, 2>(
+      spmm_unit<LPR, VPL, W, ACCUM, TWO, UU, OUTP, HINT, true, false, true, true, 2>(
           a, a.defer_list[i], li, mask, target);
     }
     return;   // the step-end barrier and the epoch advance are the next launch (k_wait)
@@ -523,11 +585,11 @@ __global__ void __launch_bounds__(BS, MINB) k_spmm(const SpmmArgs a) {
     // remote SpMM: each lane group waits for its own unit's sources first
     const bool in = u < (int64_t)a.n_tasks + a.n_groups;
     if (in && unit_wait<true>(a, u, target, li, LPR, mask))
-      spmm_unit<LPR, VPL, ACCUM, TWO, UU, OUTP, HINT, true>(a, u, li, mask);
+      spmm_unit<LPR, VPL, W, ACCUM, TWO, UU, OUTP, HINT, true>(a, u, li, mask);
     return;   // the step-end barrier and the epoch advance are the next launch (k_wait)
   }
   // two-phase without waits (loopback): coherent loads of the second source
-  spmm_unit<LPR, VPL, ACCUM, TWO, UU, OUTP, HINT, PH, PF, PH, false>(a, u, li, mask);
+  spmm_unit<LPR, VPL, W, ACCUM, TWO, UU, OUTP, HINT, PH, PF, PH, false>(a, u, li, mask);
 }
 
 // Generic width (N not a supported vector width): one warp per CSR row,
@@ -722,9 +784,11 @@ inline int64_t blocks_for(int64_t units, int rows_per_warp) {
   return (units + per_block - 1) / per_block;
 }
 
-template <int LPR, int VPL, int H, bool PF = false>
+template <int LPR, int VPL, int W, int H, bool PF = false>
 void spmm_launch(const SpmmArgs &a, bool acc, cudaStream_t s) {
-  constexpr int U = VPL == 1 ? 4 : 8;
+  // rows in flight per lane group: 4 float4 rows (N = 128, 64 registers), 8
+  // for the narrower float / float2 lanes (same registers) and wider rows
+  constexpr int U = (VPL == 1 && W == 4) ? 4 : 8;
   constexpr int BS = VPL == 1 ? 32 : 256, MINB = VPL == 1 ? 32 : 1;
   const int64_t units = a.n_tasks + a.n_groups;
   const int64_t per_cta = (int64_t)(BS / 32) * (32 / LPR);
@@ -732,27 +796,27 @@ void spmm_launch(const SpmmArgs &a, bool acc, cudaStream_t s) {
   const bool two = a.X1 != nullptr;
   if (a.ready && a.long_mid) {   // two-phase consumer (CX): stage 1 or its deferred stage 2
     if (a.cx_stage == 1) {
-      k_spmm<LPR, VPL, false, true, U, false, 0, false, BS, MINB, false, true, 1>
+      k_spmm<LPR, VPL, W, false, true, U, false, 0, false, BS, MINB, false, true, 1>
           <<<grid, BS, 0, s>>>(a);
     } else {
       const int64_t per_cta2 = (int64_t)(BS / 32) * (32 / LPR);
       const int64_t cap = ((int64_t)num_sms() * 32 * 32 / BS) ;   // one wave of lane groups
       const unsigned g2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>((units + per_cta2 - 1) / per_cta2, cap));
-      k_spmm<LPR, VPL, false, true, U, false, 0, false, BS, MINB, false, true, 2>
+      k_spmm<LPR, VPL, W, false, true, U, false, 0, false, BS, MINB, false, true, 2>
           <<<g2, BS, 0, s>>>(a);
     }
   } else if (a.ready) {   // remote SpMM with per-unit source waits, coherent loads
-    k_spmm<LPR, VPL, true, false, U, false, 0, true, BS, MINB, false, false><<<grid, BS, 0, s>>>(a);
+    k_spmm<LPR, VPL, W, true, false, U, false, 0, true, BS, MINB, false, false><<<grid, BS, 0, s>>>(a);
   } else if (a.long_mid) {   // two-phase consumer without waits (loopback)
-    k_spmm<LPR, VPL, false, true, U, false, 0, false, BS, MINB, false, true><<<grid, BS, 0, s>>>(a);
+    k_spmm<LPR, VPL, W, false, true, U, false, 0, false, BS, MINB, false, true><<<grid, BS, 0, s>>>(a);
   } else if (a.out_ptr) {   // fused exchange: overwrite rows in peer buffers
-    k_spmm<LPR, VPL, false, false, U, true, H, false, BS, MINB, PF><<<grid, BS, 0, s>>>(a);
+    k_spmm<LPR, VPL, W, false, false, U, true, H, false, BS, MINB, PF><<<grid, BS, 0, s>>>(a);
   } else if (acc) {
-    if (two) k_spmm<LPR, VPL, true, true, U, false, H, false, BS, MINB, PF><<<grid, BS, 0, s>>>(a);
-    else k_spmm<LPR, VPL, true, false, U, false, H, false, BS, MINB, PF><<<grid, BS, 0, s>>>(a);
+    if (two) k_spmm<LPR, VPL, W, true, true, U, false, H, false, BS, MINB, PF><<<grid, BS, 0, s>>>(a);
+    else k_spmm<LPR, VPL, W, true, false, U, false, H, false, BS, MINB, PF><<<grid, BS, 0, s>>>(a);
   } else {
-    if (two) k_spmm<LPR, VPL, false, true, U, false, H, false, BS, MINB, PF><<<grid, BS, 0, s>>>(a);
-    else k_spmm<LPR, VPL, false, false, U, false, H, false, BS, MINB, PF><<<grid, BS, 0, s>>>(a);
+    if (two) k_spmm<LPR, VPL, W, false, true, U, false, H, false, BS, MINB, PF><<<grid, BS, 0, s>>>(a);
+    else k_spmm<LPR, VPL, W, false, false, U, false, H, false, BS, MINB, PF><<<grid, BS, 0, s>>>(a);
   }
 }
 
@@ -775,20 +839,20 @@ bool use_prefetch(const SpmmArgs &a) {
   return false;
 }
 
-template <int LPR, int VPL>
+template <int LPR, int VPL, int W>
 void spmm_shape(const SpmmArgs &a, bool acc, cudaStream_t s) {
   if constexpr (VPL == 1 && LPR >= 8) {
     const int h = l2_hint(a);
     const bool pf = h != 2 && use_prefetch(a);
-    if (h == 2) { spmm_launch<LPR, VPL, 2>(a, acc, s); return; }
+    if (h == 2) { spmm_launch<LPR, VPL, W, 2>(a, acc, s); return; }
     if (h == 3) {
-      if (pf) spmm_launch<LPR, VPL, 3, true>(a, acc, s);
-      else spmm_launch<LPR, VPL, 3>(a, acc, s);
+      if (pf) spmm_launch<LPR, VPL, W, 3, true>(a, acc, s);
+      else spmm_launch<LPR, VPL, W, 3>(a, acc, s);
       return;
     }
-    if (pf) { spmm_launch<LPR, VPL, 0, true>(a, acc, s); return; }
+    if (pf) { spmm_launch<LPR, VPL, W, 0, true>(a, acc, s); return; }
   }
-  spmm_launch<LPR, VPL, 0>(a, acc, s);
+  spmm_launch<LPR, VPL, W, 0>(a, acc, s);
 }
 
 template <int LPR, int VPL>
@@ -854,12 +918,37 @@ int num_sms() {
   return n;
 }
 
+// SpMM lane shape for width N: LPR lanes per output row, W floats per lane
+// load, VPL loads per lane (N = LPR * W * VPL); false -> generic path.
+bool spmm_vec_shape(int N, int *lpr, int *w, int *vpl) {
+  switch (N) {
+    case 4: *lpr = 1; *w = 4; *vpl = 1; return true;
+    case 8: *lpr = 2; *w = 4; *vpl = 1; return true;
+    case 16: *lpr = 4; *w = 4; *vpl = 1; return true;
+    case 32: *lpr = 32; *w = 1; *vpl = 1; return true;
+    case 64: *lpr = 32; *w = 2; *vpl = 1; return true;
+    case 128: *lpr = 32; *w = 4; *vpl = 1; return true;
+    case 256: *lpr = 32; *w = 4; *vpl = 2; return true;
+    case 512: *lpr = 32; *w = 4; *vpl = 4; return true;
+    default: return false;
+  }
+}
+
 int launch_spmm(const SpmmArgs &a, bool accumulate, cudaStream_t s) {
   if (a.nrows == 0) return 0;
-  int lpr, vpl;
-  if (vec_shape(a.N, &lpr, &vpl)) {
+  int lpr, w, vpl;
+  if (spmm_vec_shape(a.N, &lpr, &w, &vpl)) {
     if (a.n_tasks + a.n_groups == 0) return 0;
-    SHIRO_DISPATCH(a.N, spmm_shape, a, accumulate, s);
+    switch (a.N) {
+      case 4: spmm_shape<1, 1, 4>(a, accumulate, s); break;
+      case 8: spmm_shape<2, 1, 4>(a, accumulate, s); break;
+      case 16: spmm_shape<4, 1, 4>(a, accumulate, s); break;
+      case 32: spmm_shape<32, 1, 1>(a, accumulate, s); break;
+      case 64: spmm_shape<32, 1, 2>(a, accumulate, s); break;
+      case 128: spmm_shape<32, 1, 4>(a, accumulate, s); break;
+      case 256: spmm_shape<32, 2, 4>(a, accumulate, s); break;
+      default: spmm_shape<32, 4, 4>(a, accumulate, s); break;
+    }
   } else {
     const int64_t grid = blocks_for(a.nrows, 1);
     if (accumulate)

@@ -121,8 +121,11 @@ int launch_refresh(int64_t nnz, const int32_t *vsrc, const float *V, int2 *cv, c
 // SM count of the current device (cached)
 int num_sms();
 
-// vector shape of width N: LPR lanes per row, VPL float4 per lane; false ->
-// generic (scalar) path
+// vector shape of width N for the pack / scatter kernels: LPR lanes per row,
+// VPL float4 per lane; false -> generic (scalar) path
 bool vec_shape(int N, int *lpr, int *vpl);
+// SpMM lane shape: LPR lanes per output row, W floats per lane load (1, 2, 4),
+// VPL loads per lane; N = 32 / 64 use one 32-lane group per warp
+bool spmm_vec_shape(int N, int *lpr, int *w, int *vpl);
 
 }  // namespace shiro

@@ -144,8 +144,8 @@ SplitHost make_split(const HostCsr &c, int N) {
     std::memcpy(&bits, &v, 4);
     s.cv[k] = make_int2(c.col[k], bits);
   }
-  int lpr, vpl;
-  if (!vec_shape(N, &lpr, &vpl)) return s;   // generic path: row per warp
+  int lpr, wv, vpl;
+  if (!spmm_vec_shape(N, &lpr, &wv, &vpl)) return s;   // generic path: row per warp
   mark_hot(c, N, s);
   s.L = unit_size(c.nnz());
   s.roff.assign(c.nnz(), 0);
@@ -863,9 +863,9 @@ bool inkernel_wait_enabled() {
 // (seen on 2 x B200; one GPU shared by two processes time-slices and hides it).
 bool merged_enabled(const Plan &pl) {
   const char *e = getenv("SHIRO_CX");     // read at plan time
-  int lpr, vpl;
+  int lpr, wv, vpl;
   return e && e[0] == '1' && inkernel_wait_enabled() && !(pl.flags & SHIRO_F_SPLIT_RECV) &&
-         vec_shape(pl.N, &lpr, &vpl);
+         spmm_vec_shape(pl.N, &lpr, &wv, &vpl);
 }
 
 void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
@@ -942,10 +942,10 @@ void exec_p2p(Plan &pl, const float *B, float *C, cudaStream_t s) {
   launches += stage_local(pl, B, C, s);
   rec(3, s);
   SHIRO_CK(cudaStreamWaitEvent(s, pl.ev_join, 0));
-  int lpr_, vpl_;
+  int lpr_, w_, vpl_;
   const bool split = pl.flags & SHIRO_F_SPLIT_RECV;
   if (inkernel_wait_enabled() && !split && pl.d_rem.a.n_groups + pl.d_rem.a.n_tasks > 0 &&
-      vec_shape(pl.N, &lpr_, &vpl_)) {
+      spmm_vec_shape(pl.N, &lpr_, &w_, &vpl_)) {
     DevSpmm rem = pl.d_rem;
     rem.a.ready = pl.xflags;
     rem.a.wait_epoch = ep_wait;
