@@ -319,10 +319,10 @@ int shiro_probe_gather(const float *X, int32_t N, const int32_t *idx, int64_t n_
 int shiro_probe_gather_tma(const float *X, int64_t x_rows, int32_t N, const int32_t *idx,
                            int64_t n_idx, float *out, int32_t chunk, int32_t stages, void *stream);
 
-/* Warp-specialized TMA variant (measurement only): `ctas` CTAs of 8 warps
+/* Warp-specialized TMA variant (measurement only): `ctas` CTAs of 9 warps
  * (1 producer lane issuing tile::gather4 into a `stages`-deep ring of 2 KB
- * stages, 7 consumer warps), each CTA a contiguous range of the index
- * stream.  out: device float[ctas * 7 * 128], one float4 sum per consumer
+ * stages, 8 consumer warps), each CTA a contiguous range of the index
+ * stream.  out: device float[ctas * 8 * 128], one float4 sum per consumer
  * lane (the total over `out` equals the sum of all gathered rows).  N = 128,
  * n_idx a positive multiple of 4, stages in {8, 16, 24}.
  * Errors: SHIRO_E_ARG (shape), SHIRO_E_CUDA. */

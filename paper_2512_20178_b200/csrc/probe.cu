@@ -170,20 +170,22 @@ __global__ void __launch_bounds__(256) k_probe_copy(const float4 *__restrict__ x
 }
 
 // ---- warp-specialized TMA variant (round 2): in-flight bytes decoupled from
-// warps.  CTA = 1 producer warp + 7 consumer warps, 4 CTAs per SM (32
-// resident warps, as the LDG kernel), an S-stage ring of gather4 tiles
-// (4 rows x 512 B = 2 KB per stage) per CTA: up to 4 x S x 2 KB per SM in
-// flight (S = 24: 192 KB) vs 32 warps x 4 rows x 512 B = 64 KB for LDG.128.
-// Lane 0 of warp 0 issues cp.async.bulk.tensor tile::gather4 into stage
-// q % S after the stage's EMPTY barrier; consumer warp w takes quads
-// q = w, w + 7, ... (FULL barrier with tx bytes), sums its 4 rows and
-// releases the stage.  Each CTA walks a contiguous range of quads.
+// warps.  CTA = 1 producer warp + 8 consumer warps, 4 CTAs per SM, an
+// S-stage ring of gather4 tiles (4 rows x 512 B = 2 KB per stage) per CTA: up
+// to 4 x S x 2 KB per SM in flight (S = 24: 192 KB) vs 32 warps x 4 rows x
+// 512 B = 64 KB for LDG.128.  Lane 0 of warp 0 issues cp.async.bulk.tensor
+// tile::gather4 into stage q % S after the stage's EMPTY barrier; consumer c
+// takes quads q = c, c + 8, ... -- S is a multiple of 8, so every phase of a
+// stage is awaited by the same warp in order (a parity wait on phase k while
+// phase k-1 is still pending would pass at once on the stale parity: the
+// first version, 7 consumers, deadlocked that way at full occupancy).  Each
+// CTA walks a contiguous range of quads.
 __device__ __forceinline__ void mbar_arrive(uint64_t *b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 
 template <int S>
-__global__ void __launch_bounds__(256) k_probe_gather_tma_ws(const __grid_constant__ CUtensorMap tm,
+__global__ void __launch_bounds__(288) k_probe_gather_tma_ws(const __grid_constant__ CUtensorMap tm,
                                                              const int32_t *__restrict__ idx,
                                                              int64_t nquads, int64_t n,
                                                              float *__restrict__ out) {
@@ -223,7 +225,8 @@ __global__ void __launch_bounds__(256) k_probe_gather_tma_ws(const __grid_consta
     return;
   }
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int64_t q = warp - 1; q < nq; q += 7) {
+  static_assert(S % 8 == 0, "stages must be a multiple of the 8 consumers");
+  for (int64_t q = warp - 1; q < nq; q += 8) {
     const int s = (int)(q % S);
     mbar_wait(&full[s], (uint32_t)((q / S) & 1));
 #pragma unroll
@@ -234,7 +237,7 @@ __global__ void __launch_bounds__(256) k_probe_gather_tma_ws(const __grid_consta
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
-  reinterpret_cast<float4 *>(out + ((int64_t)blockIdx.x * 7 + warp - 1) * 128)[lane] = acc;
+  reinterpret_cast<float4 *>(out + ((int64_t)blockIdx.x * 8 + warp - 1) * 128)[lane] = acc;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -336,7 +339,7 @@ extern "C" int shiro_probe_gather_tma_ws(const float *X, int64_t x_rows, int32_t
   do {                                                                                          \
     cudaFuncSetAttribute(k_probe_gather_tma_ws<S_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                          (int)smem);                                                            \
-    k_probe_gather_tma_ws<S_><<<ctas, 256, smem, s>>>(tm, idx, nq, n_idx, out);                 \
+    k_probe_gather_tma_ws<S_><<<ctas, 288, smem, s>>>(tm, idx, nq, n_idx, out);                 \
   } while (0)
   if (stages == 8) SHIRO_WS(8);
   else if (stages == 16) SHIRO_WS(16);

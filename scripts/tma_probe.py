@@ -52,7 +52,7 @@ def run(name, X, idx):
     for st in (8, 16, 24):      # warp-specialized ring, 4 CTAs x 8 warps per SM (round 2)
         variants.append((f"ws_s{st}", lambda o, st=st: sh.probe_gather_tma_ws(X, idx, o, st, 4 * sms)))
     for vname, fn in variants:
-        rows = max((n + CHUNK - 1) // CHUNK, 4 * sms * 7)
+        rows = max((n + CHUNK - 1) // CHUNK, 4 * sms * 8)
         out = torch.zeros((rows, N), device="cuda")
         ms = timeit(lambda: fn(out))
         outs[vname] = out

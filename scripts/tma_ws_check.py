@@ -14,7 +14,7 @@ ref = torch.zeros((256, 128), device="cuda")
 sh.probe_gather(X, idx, ref, 256)
 for st in (8, 16, 24):
     for ctas in (1, 4, 148 * 4):
-        out = torch.zeros((ctas * 7, 128), device="cuda")
+        out = torch.zeros((ctas * 8, 128), device="cuda")
         sh.probe_gather_tma_ws(X, idx, out, st, ctas)
         torch.cuda.synchronize()
         a, b = float(out.double().sum()), float(ref.double().sum())
