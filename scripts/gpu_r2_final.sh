@@ -13,6 +13,10 @@ if [ "$NG" = "1" ]; then
   timeout 1200 python bench.py > ${T}_bench.json 2> ${T}_bench.err
   timeout 600 python bench.py --config c2 --also none > ${T}_bench_c2.json 2> ${T}_bench_c2.err
   timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > ${T}_reference.json 2> ${T}_reference.err
+  timeout 120 python scripts/tma_ws_check.py > ${T}_tma_ws_check.txt 2>&1; echo "rc=$?" >> ${T}_tma_ws_check.txt
+  if grep -q "rc=0" ${T}_tma_ws_check.txt && ! grep -q MISMATCH ${T}_tma_ws_check.txt; then
+    timeout 1200 python scripts/tma_probe.py --configs c2 c4 c3 > ${T}_tma_probe.txt 2>&1
+  fi
   CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline"
   $CMD > ${T}_plain.log 2>&1 && \
     ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file ${T}_launches.csv $CMD > /tmp/ncu_final.log 2>&1
