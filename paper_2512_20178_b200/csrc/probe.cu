@@ -205,21 +205,28 @@ __global__ void __launch_bounds__(288) k_probe_gather_tma_ws(const __grid_consta
   }
   __syncthreads();
   if (warp == 0) {
-    if (lane == 0) {
-      for (int64_t q = 0; q < nq; ++q) {
-        const int s = (int)(q % S);
-        if (q >= S) {
-          mbar_wait(&empty[s], (uint32_t)(((q / S) - 1) & 1));
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // consumers' reads -> async writes
+    // the whole producer warp loads the indices of 8 quads at once (one
+    // coalesced 128-B load), lane 0 issues the 8 gather4s with the indices
+    // shuffled to it: the index latency is off the issue path
+    for (int64_t q8 = 0; q8 < nq; q8 += 8) {
+      const int64_t k = 4 * (q0 + q8) + lane;
+      const int idxv = __ldg(idx + (k < n ? k : n - 1));
+      for (int j = 0; j < 8; ++j) {
+        const int r0 = __shfl_sync(0xffffffffu, idxv, 4 * j + 0);
+        const int r1 = __shfl_sync(0xffffffffu, idxv, 4 * j + 1);
+        const int r2 = __shfl_sync(0xffffffffu, idxv, 4 * j + 2);
+        const int r3 = __shfl_sync(0xffffffffu, idxv, 4 * j + 3);
+        const int64_t q = q8 + j;
+        if (lane == 0 && q < nq) {
+          const int s = (int)(q % S);
+          if (q >= S) {
+            mbar_wait(&empty[s], (uint32_t)(((q / S) - 1) & 1));
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // consumers' reads -> async writes
+          }
+          mbar_expect_tx(&full[s], 4 * 512);
+          tma_gather4(ring + s * 128, &tm, &full[s], r0, r1, r2, r3);
         }
-        int r[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int64_t k = 4 * (q0 + q) + i;
-          r[i] = __ldg(idx + (k < n ? k : n - 1));
-        }
-        mbar_expect_tx(&full[s], 4 * 512);
-        tma_gather4(ring + s * 128, &tm, &full[s], r[0], r[1], r[2], r[3]);
+        __syncwarp();
       }
     }
     return;
