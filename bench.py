@@ -556,6 +556,15 @@ def measure(cfg_name, args, ctx, primary):
         if gather and dom == "local":
             roof["gather_floor_ms"] = gather["csr_stream_ms"]
             roof["gather_frac"] = round(gather["csr_stream_ms"] / dom_ms, 4)
+            # the row deliveries through L2 (one N*4-byte source row per
+            # nonzero) against the measured random-row rate of an
+            # L2-resident table: the bound of an L2-resident gather (c3)
+            l2 = gather.get("l2_random_gbs")
+            if l2:
+                got = roof["gather_bytes"] / (dom_ms * 1e-3) / 1e9
+                roof["l2_gather"] = {"achieved_gbs": round(got, 1), "peak_gbs": l2,
+                                     "frac": round(got / l2, 4),
+                                     "peak_source": "measured (gather_probe.l2_random_gbs)"}
 
     # ---- step-level roofline: T_roof = max over ranks of
     # max(HBM / BW_HBM, FLOP / FP32, NVLink / BW_NVL)
