@@ -49,8 +49,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         o = os.path.join(BUILD, os.path.basename(s) + ".o")
         objs.append(o)
         if s.endswith(".cu"):
-            sweep = ["-DSHIRO_KERNEL_SWEEP"] if os.environ.get("SHIRO_SWEEP") == "1" else []
-            cmd = [os.path.join(CUDA, "bin", "nvcc"), *ARCH, "-O3", "-lineinfo", "-std=c++17", *sweep,
+            cmd = [os.path.join(CUDA, "bin", "nvcc"), *ARCH, "-O3", "-lineinfo", "-std=c++17",
                    "-Xptxas", "-v", "-Xcompiler", "-fPIC", *common, "-c", s, "-o", o]
         else:
             cmd = ["g++", "-O2", "-g", "-std=c++17", "-fPIC", "-Wall", "-Wno-unused-function",
