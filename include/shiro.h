@@ -235,9 +235,10 @@ int shiro_spmm_host(shiro_plan_t plan, const float *B_host, float *C_host, void 
 /* A batch of nb independent SpMMs with the same plan (e.g. feature blocks or
  * GNN layers), HOST buffers: item i reads B_host[i] ([M_p x N] fp32) and
  * writes C_host[i] ([M_p x N] fp32).  Collective: every rank passes the same
- * nb.  Uploads, SpMMs and downloads are pipelined over the batch (upload of
- * item i overlaps the download of item i-1 on the full-duplex PCIe link; one
- * device copy of B and C, owned by the plan).  `stream` orders the SpMMs;
+ * nb.  Uploads, SpMMs and downloads are pipelined over the batch with two
+ * device slots of B and C owned by the plan (4 x M_p x N x 4 bytes): the
+ * upload of item i+1 and the download of item i-1 overlap the SpMM of item i
+ * (full-duplex PCIe), so an item costs max(H2D, SpMM, D2H) in steady state.  `stream` orders the SpMMs;
  * returns after every C_host[i] is written.  B_host/C_host are arrays of nb
  * host pointers (pinned memory for full bandwidth); nb = 0 is a no-op.
  * Errors: SHIRO_E_ARG (NULL arrays with nb > 0, negative nb, loopback or

@@ -34,10 +34,12 @@ Plan::~Plan() {
     if (comm_stream) cudaStreamDestroy(comm_stream);
     if (arena) cudaFree(arena);
     if (stage) cudaFree(stage);
+    if (stage2) cudaFree(stage2);
     if (vspace) cudaFree(vspace);
     if (merged_ops) cudaFree(merged_ops);
-    for (cudaEvent_t e : {ev_in, ev_comp, ev_out})
-      if (e) cudaEventDestroy(e);
+    for (int k = 0; k < 2; ++k)
+      for (cudaEvent_t e : {ev_in[k], ev_comp[k], ev_out[k]})
+        if (e) cudaEventDestroy(e);
     if (h2d_s) cudaStreamDestroy(h2d_s);
     if (d2h_s) cudaStreamDestroy(d2h_s);
     for (auto &e : prof)
@@ -1022,8 +1024,13 @@ bool graph_eligible(const Plan &pl, cudaStream_t s) {
 void launch_graph(Plan &pl, const float *B, float *C, cudaStream_t s) {
   if (pl.err_host && *pl.err_host)
     throw Error(SHIRO_E_PEER, "fused exchange: a peer did not signal in time");
-  Plan::GraphSlot &g = pl.graphs[pl.dbuf ? pl.step_parity : 0];
-  if (!g.exec || g.B != B || g.C != C || g.s != s || g.prof != pl.prof_on) {
+  const int par = pl.dbuf ? pl.step_parity : 0;
+  Plan::GraphSlot *hit = nullptr;
+  for (auto &c : pl.graphs)
+    if (c.exec && c.parity == par && c.B == B && c.C == C && c.s == s && c.prof == pl.prof_on)
+      hit = &c;
+  Plan::GraphSlot &g = hit ? *hit : pl.graphs[pl.graph_next++ % 4];
+  if (!hit) {
     if (g.exec) {
       cudaGraphExecDestroy(g.exec);
       g.exec = nullptr;
@@ -1041,6 +1048,7 @@ void launch_graph(Plan &pl, const float *B, float *C, cudaStream_t s) {
     const cudaError_t ie = cudaGraphInstantiate(&g.exec, cg, 0);
     cudaGraphDestroy(cg);
     SHIRO_CK(ie);
+    g.parity = par;
     g.B = B;
     g.C = C;
     g.s = s;
@@ -1638,36 +1646,43 @@ int shiro_spmm_host_batch(shiro_plan_t plan, int64_t nb, const float *const *B_h
     if (!pl.arena) throw Error(SHIRO_E_ARG, "plan was built with SHIRO_F_HOST_ONLY");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const size_t bytes = (size_t)pl.M * pl.N * sizeof(float);
-    if (!pl.stage && bytes) SHIRO_CK(cudaMalloc(&pl.stage, 2 * bytes));
+    if (!pl.stage2 && bytes) SHIRO_CK(cudaMalloc(&pl.stage2, 4 * bytes));   // two slots of B, C
     if (!pl.h2d_s) {
       SHIRO_CK(cudaStreamCreateWithFlags(&pl.h2d_s, cudaStreamNonBlocking));
       SHIRO_CK(cudaStreamCreateWithFlags(&pl.d2h_s, cudaStreamNonBlocking));
-      for (cudaEvent_t *e : {&pl.ev_in, &pl.ev_comp, &pl.ev_out})
-        SHIRO_CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+      for (int k = 0; k < 2; ++k)
+        for (cudaEvent_t *e : {&pl.ev_in[k], &pl.ev_comp[k], &pl.ev_out[k]})
+          SHIRO_CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
-    float *dB = pl.stage, *dC = pl.stage ? pl.stage + (size_t)pl.M * pl.N : nullptr;
-    // Pipeline over the batch with one device copy of B and C: the upload of
-    // B[i] waits only for SpMM i-1 to finish reading dB, and overlaps the
-    // download of C[i-1] (PCIe is full duplex); SpMM i waits for its upload
-    // and for the download of C[i-1] to finish reading dC.  Steady state per
-    // item: max(H2D, D2H) + the SpMM.
-    SHIRO_CK(cudaEventRecord(pl.ev_comp, s));
-    SHIRO_CK(cudaEventRecord(pl.ev_out, s));
+    const size_t elems = (size_t)pl.M * pl.N;
+    auto dB = [&](int k) { return pl.stage2 ? pl.stage2 + (2 * k) * elems : nullptr; };
+    auto dC = [&](int k) { return pl.stage2 ? pl.stage2 + (2 * k + 1) * elems : nullptr; };
+    // Double-buffered pipeline over the batch: item i uses slot k = i mod 2.
+    // The upload of B[i] waits only for SpMM i-2 (the last reader of slot k),
+    // so it overlaps SpMM i-1; SpMM i waits for its upload and for the
+    // download of C[i-2] (the last reader of dC[k]); the download of C[i]
+    // overlaps SpMM i+1 and the upload of B[i+2] (PCIe is full duplex).
+    // Steady state per item: max(H2D, SpMM, D2H) instead of their sum.
+    for (int k = 0; k < 2; ++k) {
+      SHIRO_CK(cudaEventRecord(pl.ev_comp[k], s));
+      SHIRO_CK(cudaEventRecord(pl.ev_out[k], s));
+    }
     int64_t launches = 0;
     for (int64_t i = 0; i < nb; ++i) {
-      SHIRO_CK(cudaStreamWaitEvent(pl.h2d_s, pl.ev_comp, 0));
-      if (bytes) SHIRO_CK(cudaMemcpyAsync(dB, B_host[i], bytes, cudaMemcpyHostToDevice, pl.h2d_s));
-      SHIRO_CK(cudaEventRecord(pl.ev_in, pl.h2d_s));
-      SHIRO_CK(cudaStreamWaitEvent(s, pl.ev_in, 0));
-      SHIRO_CK(cudaStreamWaitEvent(s, pl.ev_out, 0));
-      run_step(pl, dB, dC, s);
+      const int k = (int)(i & 1);
+      SHIRO_CK(cudaStreamWaitEvent(pl.h2d_s, pl.ev_comp[k], 0));
+      if (bytes) SHIRO_CK(cudaMemcpyAsync(dB(k), B_host[i], bytes, cudaMemcpyHostToDevice, pl.h2d_s));
+      SHIRO_CK(cudaEventRecord(pl.ev_in[k], pl.h2d_s));
+      SHIRO_CK(cudaStreamWaitEvent(s, pl.ev_in[k], 0));
+      SHIRO_CK(cudaStreamWaitEvent(s, pl.ev_out[k], 0));
+      run_step(pl, dB(k), dC(k), s);
       launches += pl.last_launches;
-      SHIRO_CK(cudaEventRecord(pl.ev_comp, s));
-      SHIRO_CK(cudaStreamWaitEvent(pl.d2h_s, pl.ev_comp, 0));
-      if (bytes) SHIRO_CK(cudaMemcpyAsync(C_host[i], dC, bytes, cudaMemcpyDeviceToHost, pl.d2h_s));
-      SHIRO_CK(cudaEventRecord(pl.ev_out, pl.d2h_s));
+      SHIRO_CK(cudaEventRecord(pl.ev_comp[k], s));
+      SHIRO_CK(cudaStreamWaitEvent(pl.d2h_s, pl.ev_comp[k], 0));
+      if (bytes) SHIRO_CK(cudaMemcpyAsync(C_host[i], dC(k), bytes, cudaMemcpyDeviceToHost, pl.d2h_s));
+      SHIRO_CK(cudaEventRecord(pl.ev_out[k], pl.d2h_s));
     }
-    SHIRO_CK(cudaStreamWaitEvent(s, pl.ev_out, 0));
+    for (int k = 0; k < 2; ++k) SHIRO_CK(cudaStreamWaitEvent(s, pl.ev_out[k], 0));
     SHIRO_CK(cudaStreamSynchronize(s));
     if (pl.err_host && *pl.err_host)
       throw Error(SHIRO_E_PEER, "fused exchange: a peer did not signal in time (C is invalid)");

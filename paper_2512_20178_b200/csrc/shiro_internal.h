@@ -208,17 +208,21 @@ struct Plan {
   // CUDA graph of one step (P = 1, fused exchange, hierarchical), keyed by
   // (B, C, stream, profiling); replayed while the key matches
   struct GraphSlot {
+    int parity = -1;
     cudaGraphExec_t exec = nullptr;
     const float *B = nullptr;
     float *C = nullptr;
     cudaStream_t s = nullptr;
     bool prof = false;
     int64_t launches = 0;
-  } graphs[2];                        // one per step parity (double buffering)
-  // device staging of B and C for shiro_spmm_host / shiro_spmm_host_batch
-  float *stage = nullptr;
+  } graphs[4];                        // keyed by (step parity, B, C, stream): both
+                                      // parities x both host-batch staging slots
+  int graph_next = 0;                 // round-robin replacement
+  // device staging of B and C for shiro_spmm_host (stage) and the
+  // double-buffered shiro_spmm_host_batch (stage2: two slots of B and C)
+  float *stage = nullptr, *stage2 = nullptr;
   cudaStream_t h2d_s = nullptr, d2h_s = nullptr;   // copy engines of the batch pipeline
-  cudaEvent_t ev_in = nullptr, ev_comp = nullptr, ev_out = nullptr;
+  cudaEvent_t ev_in[2] = {}, ev_comp[2] = {}, ev_out[2] = {};
   // value refresh (N3): value space V = [local values || row-based values
   // received from each peer, peers ascending]; every device op's nonzeros
   // map into it (vsrc)
