@@ -47,6 +47,13 @@ def lib_digests(pl, P):
     return out
 
 
+def test_c5_config_describes_its_matrix():
+    """The config's nnz is the distinct-entry count of its 2^30 samples."""
+    rp, col, val = c5()
+    assert int(rp[-1]) == shiro_gen.CONFIGS["c5"].nnz
+    assert shiro_gen.CONFIGS["c5"].samples == 1 << 30
+
+
 @pytest.mark.parametrize("P", [2, 4, 8])
 def test_c5_plan_digests(P):
     cfg = shiro_gen.CONFIGS["c5"]

@@ -19,7 +19,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, cfg, bad_rank, out_q):
+def _worker(rank, world, port, cfg, bad_rank, out_q, weighted=False):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -37,13 +37,20 @@ def _worker(rank, world, port, cfg, bad_rank, out_q):
         vl = val[row_ptr[lo]:row_ptr[hi]]
         if rank == bad_rank and cl.size:
             cl[0] = c.n + 5                          # out of range column
+        w = {}
+        if weighted:      # N2: per-vertex costs (C rows of this rank, every B row)
+            rng = np.random.default_rng(3)
+            wr, wc = rng.integers(1, 9, c.n), rng.integers(1, 9, c.n)
+            w = dict(w_row=wr[lo:hi], w_col=wc)
         try:
             pl = sh.Plan.distributed(rank, world, c.n, part, rp, cl, vl, c.N,
-                                     flags=sh.F_HOST_ONLY, host_xchg=sh.torch_dist_alltoallv())
+                                     flags=sh.F_HOST_ONLY, host_xchg=sh.torch_dist_alltoallv(),
+                                     **w)
         except sh.ShiroError as e:
             out_q.put((rank, "error", e.code))
             return
-        op = oracle.plan_flat(c.n, part, row_ptr, col)
+        op = oracle.plan_flat(c.n, part, row_ptr, col,
+                              **({"w_row": wr, "w_col": wc} if weighted else {}))
         ok = True
         empty = np.empty(0, np.int64)
         for p in range(world):
@@ -61,11 +68,11 @@ def _worker(rank, world, port, cfg, bad_rank, out_q):
         dist.destroy_process_group()
 
 
-def _run(world, cfg, bad_rank=-1):
+def _run(world, cfg, bad_rank=-1, weighted=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, bad_rank, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, bad_rank, q, weighted))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -78,6 +85,13 @@ def _run(world, cfg, bad_rank=-1):
 @pytest.mark.parametrize("world", [2, 4])
 def test_gloo_distributed_plan_matches_oracle(world):
     res = _run(world, "c1")
+    assert all(r[1] == "ok" for r in res), res
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_weighted_plan_matches_oracle(world):
+    """Weighted covers (N2) planned by separate processes over gloo."""
+    res = _run(world, "c1", weighted=True)
     assert all(r[1] == "ok" for r in res), res
 
 
