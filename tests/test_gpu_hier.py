@@ -84,6 +84,7 @@ def test_graph_replay_matches_direct_launch():
     ref = oracle.spmm_ref(row_ptr, col, val, B)
     for _ in range(3):
         Cd = torch.full((c.n, c.N), float("nan"), device="cuda")
+        st.wait_stream(torch.cuda.current_stream())   # C's fill first
         pl.spmm(Bd, Cd, st)
         st.synchronize()
         assert np.array_equal(Cd.cpu().numpy().astype(np.float64), ref)

@@ -70,6 +70,7 @@ def _worker(rank, world, port, flags, g, cfg_name, env, out_q):
             ref = oracle.spmm_ref(row_ptr, col, vi, Bfull, rows=np.arange(lo, hi))
             Bd = torch.from_numpy(B).cuda()
             Cd = torch.full((hi - lo, c.N), float("nan"), device="cuda")
+            stream.wait_stream(torch.cuda.current_stream())   # B's copy and C's fill first
             pl.spmm(Bd, Cd, stream)
             stream.synchronize()
             bad += int((Cd.cpu().numpy().astype(np.float64) != ref).sum())

@@ -125,6 +125,7 @@ def _worker(rank, world, port, case, out_q):
                 return
             Bd = torch.from_numpy(B[lo:hi].copy()).cuda()
             Cd = torch.full((hi - lo, N), float("nan"), device="cuda")
+            stream.wait_stream(torch.cuda.current_stream())   # B's copy and C's fill first
             with torch.cuda.stream(stream):
                 pl.spmm(Bd, Cd, stream)
             stream.synchronize()
