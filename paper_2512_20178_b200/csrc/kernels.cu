@@ -9,7 +9,8 @@
 //     with one 128-bit load per lane (fully coalesced LDG.128);
 //   * the nonzeros of a work unit are loaded cooperatively as interleaved
 //     (col, val) pairs, one 8-byte streaming load per lane, and broadcast with
-//     shuffles; U = 4 independent row gathers are issued before any FMA;
+//     shuffles; U = 8 independent row gathers are issued before any FMA
+//     (the value of each is shuffled at its FMA, holding no register);
 //   * short rows are packed at plan time into row groups (<= L nonzeros,
 //     <= 64 rows); a per-nonzero byte gives the row offset inside the group,
 //     so row boundaries cost no memory access and the gathers of many short
@@ -20,7 +21,9 @@
 //     single launch;
 //   * fp32 accumulation in registers, one store per output row;
 //   * one-warp CTAs, 32 resident per SM (measured best).
-// L2 policy per launch (HINT): 0 default; 2 = source rows fit in L2 -> the
+// L2 policy per launch (HINT): 0 default; 1 = the streams evict_first, the
+// gathers default; 4 = as 3 with the compact hot buffer (X1) as the hot
+// rows; 2 = source rows fit in L2 -> the
 // streams (A's (col, val) pairs, C rows) evict_first, gathered rows
 // evict_last; 3 = source rows far larger than L2 -> the plan-time "hot" rows
 // (bit 31 of the column id) evict_last, every other gather and the streams
@@ -141,7 +144,9 @@ __device__ __forceinline__ void st_pol(float4 *p, const float4 &v, uint64_t pol)
                : "memory");
 }
 
-// gathered source row: HINT 0 plain LDG; 2 evict_last; 3 evict_last for hot
+// gathered source row: HINT 0 and 1 plain LDG (1 only marks the streams --
+// column/value words, row offsets, output rows -- evict_first); 2 evict_last;
+// 4 evict_last for the compact hot buffer (X1), evict_first otherwise; 3 evict_last for hot
 // rows, evict_first otherwise; COH (and coh for this row): a weak
 // (coherent-path, L1-cacheable) load instead of the read-only ld.global.nc:
 // peers store into other parts of the buffer during the launch, and these
@@ -150,7 +155,7 @@ __device__ __forceinline__ void st_pol(float4 *p, const float4 &v, uint64_t pol)
 template <int HINT, bool COH, typename V>
 __device__ __forceinline__ V ldB(const V *p, bool hot, bool coh) {
   if (COH && coh) return ld_weak(p);
-  if (HINT == 0) return __ldg(p);
+  if (HINT <= 1) return __ldg(p);
   // the policy operand lives in a uniform register: one load per constant
   // policy (a per-row select would make the compiler waterfall over lanes);
   // `hot` is uniform across the lane group, so this branch never diverges
@@ -183,8 +188,16 @@ __device__ __forceinline__ void add4(float4 &acc, const float4 &x) {
 // (one IMAD.WIDE.U32 per row: column ids and N are non-negative 32-bit)
 template <bool TWO>
 __device__ __forceinline__ const float *src_row_ptr(const SpmmArgs &a, int c) {
-  if (TWO && c >= a.n0) return a.X1 + (uint64_t)(uint32_t)(c - (int)a.n0) * (uint32_t)a.N;
-  return a.X0 + (uint64_t)(uint32_t)c * (uint32_t)a.N;
+  const uint32_t rowb = (uint32_t)a.N * 4u;
+  if (TWO) {
+    // branch-free: one select of the base, X1's rows addressed as
+    // (X1 - n0 rows) + c rows (a per-gather branch cost 1.5x the instructions)
+    const uint64_t b1 = reinterpret_cast<uint64_t>(a.X1) - (uint64_t)a.n0 * rowb;
+    const uint64_t base = (c >= a.n0) ? b1 : reinterpret_cast<uint64_t>(a.X0);
+    return reinterpret_cast<const float *>(base + (uint64_t)(uint32_t)c * rowb);
+  }
+  return reinterpret_cast<const float *>(reinterpret_cast<uint64_t>(a.X0) +
+                                         (uint64_t)(uint32_t)c * rowb);
 }
 template <bool TWO, typename V>
 __device__ __forceinline__ const V *src_row(const SpmmArgs &a, int c) {
@@ -252,26 +265,25 @@ __device__ __forceinline__ V *out_addr(const SpmmArgs &a, long long v) {
 // Gather U source rows for nonzeros j..j+U-1 of the current batch; the
 // weights are broadcast together with the columns, before any FMA.
 template <int LPR, int VPL, int W, bool TWO, int U, int HINT, bool COH>
-__device__ __forceinline__ void gather(const SpmmArgs &a, typename VT<W>::T (&x)[U][VPL], float (&w)[U],
-                                       int c, float v, int j, int cnt, int li, unsigned mask) {
+__device__ __forceinline__ void gather(const SpmmArgs &a, typename VT<W>::T (&x)[U][VPL], int c, int j,
+                                       int cnt, int li, unsigned mask) {
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const int cu = __shfl_sync(mask, c, j + u, LPR);
-    const float vu = __shfl_sync(mask, v, j + u, LPR);
     if (j + u < cnt) {               // uniform across the lane group
       // hot marks (bit 31) exist only in HINT 3 launches
       const typename VT<W>::T *r = src_row<TWO, typename VT<W>::T>(a, HINT == 3 ? (cu & 0x7fffffff) : cu);
       // with two sources only the second one (the receive buffer) is written
       // by peers during the launch
       const bool coh = !TWO || cu >= a.n0;
+      // evict_last: marked rows (HINT 3) or the compact hot buffer (HINT 4, X1)
+      const bool hot = (HINT == 3 && cu < 0) || (HINT == 4 && cu >= a.n0);
 #pragma unroll
       for (int q = 0; q < VPL; ++q)
-        x[u][q] = ldB<HINT, COH>(r + li + q * LPR, HINT == 3 && cu < 0, coh);
-      w[u] = vu;
+        x[u][q] = ldB<HINT, COH>(r + li + q * LPR, hot, coh);
     } else {
 #pragma unroll
       for (int q = 0; q < VPL; ++q) x[u][q] = VT<W>::zero();
-      w[u] = 0.f;
     }
   }
 }
@@ -344,12 +356,15 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
         const int cnt = (int)((k1 - base) < LPR ? (k1 - base) : LPR);
         for (int j = 0; j < cnt; j += U) {
           typename VT<W>::T x[U][VPL];
-          float w[U];
-          gather<LPR, VPL, W, TWO, U, HINT, COH>(a, x, w, cv.x, __int_as_float(cv.y), j, cnt, li, mask);
+          gather<LPR, VPL, W, TWO, U, HINT, COH>(a, x, cv.x, j, cnt, li, mask);
 #pragma unroll
-          for (int uu = 0; uu < U; ++uu)
+          for (int uu = 0; uu < U; ++uu) {
+            // the weight is shuffled at use: no register held per row in flight
+            // (lanes past cnt hold v = 0 and x = 0)
+            const float wu = __shfl_sync(mask, __int_as_float(cv.y), j + uu, LPR);
 #pragma unroll
-            for (int q = 0; q < VPL; ++q) fma4(acc[q], w[uu], x[uu][q]);
+            for (int q = 0; q < VPL; ++q) fma4(acc[q], wu, x[uu][q]);
+          }
         }
       }
     };
@@ -468,15 +483,15 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
     const int cnt = (int)((kend - base) < LPR ? (kend - base) : LPR);
     for (int j = 0; j < cnt; j += U) {
       typename VT<W>::T x[U][VPL];
-      float w[U];
-      gather<LPR, VPL, W, TWO, U, HINT, COH>(a, x, w, cv.x, __int_as_float(cv.y), j, cnt, li, mask);
+      gather<LPR, VPL, W, TWO, U, HINT, COH>(a, x, cv.x, j, cnt, li, mask);
 #pragma unroll
       for (int uu = 0; uu < U; ++uu) {
         const int rou = __shfl_sync(mask, ro, j + uu, LPR);
+        const float wu = __shfl_sync(mask, __int_as_float(cv.y), j + uu, LPR);
         if (j + uu < cnt) {
           while (cur < rou) flush();        // finished rows (and empty rows)
 #pragma unroll
-          for (int q = 0; q < VPL; ++q) fma4(acc[q], w[uu], x[uu][q]);
+          for (int q = 0; q < VPL; ++q) fma4(acc[q], wu, x[uu][q]);
         }
       }
     }
@@ -523,18 +538,18 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, const int64_t u, co
     const int cnt = (int)((g.k1 - base) < LPR ? (g.k1 - base) : LPR);
     for (int j = 0; j < cnt; j += U) {
       typename VT<W>::T x[U][VPL];
-      float w[U];
-      gather<LPR, VPL, W, TWO, U, HINT, COH>(a, x, w, cv.x, __int_as_float(cv.y), j, cnt, li, mask);
+      gather<LPR, VPL, W, TWO, U, HINT, COH>(a, x, cv.x, j, cnt, li, mask);
 #pragma unroll
       for (int uu = 0; uu < U; ++uu) {
         const int rou = __shfl_sync(mask, ro, j + uu, LPR);
+        const float wu = __shfl_sync(mask, __int_as_float(cv.y), j + uu, LPR);
         if (j + uu < cnt) {
           if (rou != rcur) {
             if (rcur >= 0) flush_b();
             rcur = rou;
           }
 #pragma unroll
-          for (int q = 0; q < VPL; ++q) fma4(acc[q], w[uu], x[uu][q]);
+          for (int q = 0; q < VPL; ++q) fma4(acc[q], wu, x[uu][q]);
         }
       }
     }
@@ -784,11 +799,13 @@ inline int64_t blocks_for(int64_t units, int rows_per_warp) {
   return (units + per_block - 1) / per_block;
 }
 
-template <int LPR, int VPL, int W, int H, bool PF = false>
+template <int LPR, int VPL, int W, int H, bool PF = false, int UO = 0>
 void spmm_launch(const SpmmArgs &a, bool acc, cudaStream_t s) {
-  // rows in flight per lane group: 4 float4 rows (N = 128, 64 registers), 8
-  // for the narrower float / float2 lanes (same registers) and wider rows
-  constexpr int U = (VPL == 1 && W == 4) ? 4 : 8;
+  // rows in flight per lane group: 8 (N = 128: 8 float4 rows in 64 registers
+  // since the weights are shuffled at use, measured 3-7 % faster than 4 on
+  // c3 / c4; N = 64: 8 float2 -- 16 was 29 % slower on c5); 4 for the
+  // narrow float4 lane groups (N = 4..16)
+  constexpr int U = UO ? UO : ((VPL == 1 && W == 4 && LPR < 32) ? 4 : 8);
   constexpr int BS = VPL == 1 ? 32 : 256, MINB = VPL == 1 ? 32 : 1;
   const int64_t units = a.n_tasks + a.n_groups;
   const int64_t per_cta = (int64_t)(BS / 32) * (32 / LPR);
@@ -821,13 +838,16 @@ void spmm_launch(const SpmmArgs &a, bool acc, cudaStream_t s) {
 }
 
 // L2 policy of a launch (SHIRO_L2HINT overrides): 3 when the op carries hot
-// marks, 2 when its source rows fit comfortably in L2 (c2: B = 87 MB, -5 %),
-// else 0 (profiles/r1_kernel_sweep.txt, "L2 hints").
+// marks, 4 with a compact hot buffer, 2 when its source rows fit comfortably
+// in L2 (c2: B = 87 MB, -5 %, profiles/r1_kernel_sweep.txt), else 1 (the
+// streams evict_first: c3 / c4 / c5 -0.4 / -0.5 / -2.2 %, profiles/r2_hotbuf_sweep.txt).
 int l2_hint(const SpmmArgs &a) {
   static const int env_hint = getenv("SHIRO_L2HINT") ? atoi(getenv("SHIRO_L2HINT")) : -1;
-  if (env_hint >= 0) return (env_hint == 3 && !a.hot) ? 0 : env_hint;
-  if (a.hot) return 3;
-  return (a.X1 == nullptr && a.n0 * (int64_t)a.N * 4 <= (96ll << 20)) ? 2 : 0;
+  static const int hb_pol = getenv("SHIRO_HOTBUF_POL") ? atoi(getenv("SHIRO_HOTBUF_POL")) : 1;
+  if (a.hot == 2 && a.X1) return hb_pol ? 4 : 0;   // compact hot buffer
+  if (env_hint >= 0) return (env_hint == 3 && a.hot != 1) ? 0 : env_hint;
+  if (a.hot == 1) return 3;
+  return (a.X1 == nullptr && a.n0 * (int64_t)a.N * 4 <= (96ll << 20)) ? 2 : 1;
 }
 
 // L2 prefetch of each batch's source rows (SHIRO_PREFETCH: 1 on, 0 off; by
@@ -844,7 +864,19 @@ void spmm_shape(const SpmmArgs &a, bool acc, cudaStream_t s) {
   if constexpr (VPL == 1 && LPR >= 8) {
     const int h = l2_hint(a);
     const bool pf = h != 2 && use_prefetch(a);
+    if constexpr (W >= 2 && LPR == 32) {   // SHIRO_U128=4 / SHIRO_U64=4: 4 rows in flight (A/B)
+      static const bool u4 = getenv(W == 4 ? "SHIRO_U128" : "SHIRO_U64") &&
+                             atoi(getenv(W == 4 ? "SHIRO_U128" : "SHIRO_U64")) == 4;
+      if (u4 && h <= 2) {
+        if (h == 2) spmm_launch<LPR, VPL, W, 2, false, 4>(a, acc, s);
+        else if (h == 1) spmm_launch<LPR, VPL, W, 1, false, 4>(a, acc, s);
+        else spmm_launch<LPR, VPL, W, 0, false, 4>(a, acc, s);
+        return;
+      }
+    }
     if (h == 2) { spmm_launch<LPR, VPL, W, 2>(a, acc, s); return; }
+    if (h == 1) { spmm_launch<LPR, VPL, W, 1>(a, acc, s); return; }
+    if (h == 4) { spmm_launch<LPR, VPL, W, 4>(a, acc, s); return; }
     if (h == 3) {
       if (pf) spmm_launch<LPR, VPL, W, 3, true>(a, acc, s);
       else spmm_launch<LPR, VPL, W, 3>(a, acc, s);

@@ -51,7 +51,8 @@ struct SpmmArgs {
   const int32_t *long_first = nullptr;  // [n_long+1] first task of each long row
   int32_t *long_counter = nullptr;      // [n_long] zero-initialised arrival counters
   float *scratch = nullptr;             // [n_tasks * N] chunk partials
-  int32_t hot = 0;                      // 1: cv carries kHotBit marks (hot/cold L2 policy)
+  int32_t hot = 0;                      // 1: cv carries kHotBit marks (hot/cold L2 policy);
+                                        // 2: X1 is the op's compact hot buffer
   // Two-phase op (fused-exchange consumer CX): each row's nonzeros are its
   // local part (columns < n0, source X0 = B_local) then its remote part
   // (columns >= n0, X1 = receive buffer); long_mid[l] = first remote nonzero

@@ -103,6 +103,8 @@ struct SplitHost {
   std::vector<uint64_t> unit_src;   // per unit (tasks, then groups): source mask
   std::vector<int32_t> vsrc;        // refresh map in cv order (two-phase ops permute)
   std::vector<int64_t> long_mid;    // two-phase ops: first remote nonzero of each long row
+  std::vector<int32_t> hot_ids;     // compact hot buffer: its source rows (slot order)
+  std::vector<int32_t> hot_dst;     // ... and their slots 0..H-1 (k_pack destinations)
   bool hot = false;
 };
 
@@ -115,11 +117,13 @@ int64_t env_mb(const char *name, int64_t dflt) {
 // L2, the most referenced source rows (column degree >= 2, highest first, up
 // to SHIRO_HOT_MB of rows) are marked so that their gathers are L2
 // evict_last and every other gather evict_first.
-void mark_hot(const HostCsr &c, int N, SplitHost &s) {
+// The most referenced source rows of an op (column degree >= 2, highest
+// first, ties by id) up to `budget` bytes of rows, when its source rows are
+// more than SHIRO_HOT_MIN_MB (default 96 MB, i.e. far from L2-resident).
+std::vector<int32_t> select_hot(const HostCsr &c, int N, int64_t budget) {
   const int64_t rowb = (int64_t)N * 4;
-  const int64_t budget = env_mb("SHIRO_HOT_MB", 0) << 20;
   const int64_t min_src = env_mb("SHIRO_HOT_MIN_MB", 96) << 20;
-  if (c.hot_rows <= 0 || budget <= 0 || c.hot_rows * rowb <= min_src || c.nnz() == 0) return;
+  if (c.hot_rows <= 0 || budget <= 0 || c.hot_rows * rowb <= min_src || c.nnz() == 0) return {};
   std::vector<int32_t> deg(c.hot_rows, 0);
   for (int32_t j : c.col)
     if (j >= 0 && j < c.hot_rows) deg[j]++;
@@ -130,11 +134,40 @@ void mark_hot(const HostCsr &c, int N, SplitHost &s) {
   std::partial_sort(ids.begin(), ids.begin() + H, ids.end(), [&](int32_t a, int32_t b) {
     return deg[a] != deg[b] ? deg[a] > deg[b] : a < b;
   });
+  ids.resize(H);
+  return ids;
+}
+
+void mark_hot(const HostCsr &c, int N, SplitHost &s) {
+  const std::vector<int32_t> ids = select_hot(c, N, env_mb("SHIRO_HOT_MB", 0) << 20);
+  if (ids.empty()) return;
   std::vector<uint8_t> hot(c.hot_rows, 0);
-  for (size_t i = 0; i < H; ++i) hot[ids[i]] = 1;
+  for (int32_t j : ids) hot[j] = 1;
   for (int64_t k = 0; k < c.nnz(); ++k)
     if (c.col[k] >= 0 && c.col[k] < c.hot_rows && hot[c.col[k]]) s.cv[k].x |= kHotBit;
-  s.hot = H > 0;
+  s.hot = true;
+}
+
+// Compact hot buffer (SHIRO_HOTBUF_MB, single-source ops only): the hot
+// source rows are copied each step into a contiguous buffer (one k_pack of
+// hot_ids) that the op reads as its second source -- column j of a hot row
+// becomes hot_rows + slot -- so an address-based L2 policy (the in-kernel
+// evict_last of HINT 4, or a persisting access-policy window) covers exactly
+// them, and the hot gathers share few pages.
+void make_hotbuf(const HostCsr &c, int N, SplitHost &s) {
+  if (s.hot || !c.mid.empty() || !c.src_bounds.empty() || !c.out_row.empty() || c.ptr_rows) return;
+  s.hot_ids = select_hot(c, N, env_mb("SHIRO_HOTBUF_MB", 0) << 20);
+  if (s.hot_ids.empty()) return;
+  if (c.hot_rows + (int64_t)s.hot_ids.size() > 0x7fffffffLL) {   // ids stay int32
+    s.hot_ids.clear();
+    return;
+  }
+  std::vector<int32_t> slot(c.hot_rows, -1);
+  for (size_t i = 0; i < s.hot_ids.size(); ++i) slot[s.hot_ids[i]] = (int32_t)i;
+  for (int64_t k = 0; k < c.nnz(); ++k) {
+    const int32_t j = c.col[k];
+    if (j >= 0 && j < c.hot_rows && slot[j] >= 0) s.cv[k].x = (int32_t)(c.hot_rows + slot[j]);
+  }
 }
 
 SplitHost make_split(const HostCsr &c, int N) {
@@ -149,6 +182,7 @@ SplitHost make_split(const HostCsr &c, int N) {
   int lpr, wv, vpl;
   if (!spmm_vec_shape(N, &lpr, &wv, &vpl)) return s;   // generic path: row per warp
   mark_hot(c, N, s);
+  make_hotbuf(c, N, s);
   s.L = unit_size(c.nnz());
   s.roff.assign(c.nnz(), 0);
   const int64_t max_rows = (c.out_row.empty() && !c.ptr_rows) ? kMaxGroupRows
@@ -240,7 +274,7 @@ SplitHost make_split(const HostCsr &c, int N) {
 }
 
 struct SpmmLayout {
-  size_t rp, cv, roff, out, tl, lrow, lfirst, cnt, scratch, grp, usrc, vsrc, lmid;
+  size_t rp, cv, roff, out, tl, lrow, lfirst, cnt, scratch, grp, usrc, vsrc, lmid, hsrc, hdst, hbuf;
   SplitHost sp;
   bool has_out, has_usrc, has_vsrc;
 };
@@ -266,6 +300,12 @@ SpmmLayout layout_spmm(Arena &ar, const HostCsr &c, int N) {
     throw Error(SHIRO_E_INTERNAL, "refresh map size");
   L.vsrc = put(ar, L.sp.vsrc.empty() ? c.vsrc : L.sp.vsrc);
   L.lmid = put(ar, L.sp.long_mid);
+  // (the arena keeps pointers to the host vectors until upload: they live in L.sp)
+  L.sp.hot_dst.resize(L.sp.hot_ids.size());
+  for (size_t i = 0; i < L.sp.hot_dst.size(); ++i) L.sp.hot_dst[i] = (int32_t)i;
+  L.hsrc = put(ar, L.sp.hot_ids);
+  L.hdst = put(ar, L.sp.hot_dst);
+  L.hbuf = ar.reserve(L.sp.hot_ids.size() * (size_t)N * sizeof(float));
   return L;
 }
 
@@ -292,6 +332,14 @@ DevSpmm bind_spmm(char *base, const SpmmLayout &L, const HostCsr &c, int N) {
   d.nnz = c.nnz();
   d.vsrc = L.has_vsrc ? reinterpret_cast<const int32_t *>(base + L.vsrc) : nullptr;
   a.long_mid = c.mid.empty() ? nullptr : reinterpret_cast<const int64_t *>(base + L.lmid);
+  if (!L.sp.hot_ids.empty()) {
+    d.hot.n = (int64_t)L.sp.hot_ids.size();
+    d.hot.src = reinterpret_cast<const int32_t *>(base + L.hsrc);
+    d.hot.dst = reinterpret_cast<const int32_t *>(base + L.hdst);
+    d.hot_buf = reinterpret_cast<float *>(base + L.hbuf);
+    d.hot_base = c.hot_rows;
+    a.hot = 2;
+  }
   return d;
 }
 
@@ -593,12 +641,38 @@ void refresh_device(Plan &pl, const std::vector<float> &V, cudaStream_t s) {
 
 namespace {
 
+// SHIRO_HOTBUF_WIN=1: a persisting L2 access-policy window over the compact
+// hot buffer around its op's launch (measurement knob)
+bool hotbuf_window() {
+  static const int v = getenv("SHIRO_HOTBUF_WIN") ? atoi(getenv("SHIRO_HOTBUF_WIN")) : 0;
+  return v == 1;
+}
+
 int64_t run_spmm(const DevSpmm &d, const float *X0, int64_t n0, const float *X1, float *Y,
                  bool accumulate, cudaStream_t s) {
   if (d.a.nrows == 0) return 0;
   SpmmArgs a = d.a;
   a.X0 = X0; a.n0 = n0; a.X1 = X1; a.Y = Y;
-  return launch_spmm(a, accumulate, s);
+  int64_t n = 0;
+  if (d.hot.n) {   // compact hot buffer: this step's hot rows of X0, then the op reads it as X1
+    if (X1 || n0 != d.hot_base) throw Error(SHIRO_E_INTERNAL, "hot buffer op with a second source");
+    n += launch_pack(d.hot.n, d.hot.src, d.hot.dst, X0, d.hot_buf, a.N, s);
+    a.X1 = d.hot_buf;
+    if (hotbuf_window()) {
+      cudaStreamAttrValue v = {};
+      v.accessPolicyWindow.base_ptr = d.hot_buf;
+      v.accessPolicyWindow.num_bytes = (size_t)d.hot.n * a.N * sizeof(float);
+      v.accessPolicyWindow.hitRatio = 1.0f;
+      v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      SHIRO_CK(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v));
+      n += launch_spmm(a, accumulate, s);
+      v.accessPolicyWindow.num_bytes = 0;
+      SHIRO_CK(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v));
+      return n;
+    }
+  }
+  return n + launch_spmm(a, accumulate, s);
 }
 
 // E1 + E2: fill the send buffer from B

@@ -66,16 +66,18 @@ struct HostCsr {
 };
 
 // Device image of a SpMM op (arrays live in the plan's arena)
-struct DevSpmm {
-  SpmmArgs a;            // pointers to device arrays; X/Y filled at run time
-  int64_t nnz = 0;
-  const int32_t *vsrc = nullptr;   // refresh map (nnz entries) or nullptr
-};
-
 // Device image of a gather (pack) or gather-sum (scatter) op
 struct DevPack {
   int64_t n = 0;
   const int32_t *src = nullptr, *dst = nullptr;
+};
+struct DevSpmm {
+  SpmmArgs a;            // pointers to device arrays; X/Y filled at run time
+  int64_t nnz = 0;
+  const int32_t *vsrc = nullptr;   // refresh map (nnz entries) or nullptr
+  DevPack hot;                     // compact hot buffer: rows of X0 copied each step
+  float *hot_buf = nullptr;        // ... into this buffer, read as X1 (columns >= hot_base)
+  int64_t hot_base = 0;
 };
 struct DevScatter {
   int64_t nt = 0;

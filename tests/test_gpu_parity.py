@@ -144,6 +144,36 @@ def test_loopback_two_phase_consumer_exact(P, N, monkeypatch):
     assert np.array_equal(C.astype(np.float64), oracle.spmm_ref(row_ptr, col, val, B))
 
 
+@pytest.mark.parametrize("P", [1, 2, 4])
+@pytest.mark.parametrize("N", [32, 64, 128])
+def test_compact_hot_buffer_exact(P, N, monkeypatch):
+    """The compact hot buffer (SHIRO_HOTBUF_MB): the most
+    referenced source rows of the local op are copied each step into a
+    contiguous buffer read as the op's second source; integer data exact,
+    one extra launch (the copy) at P = 1."""
+    monkeypatch.setenv("SHIRO_HOTBUF_MB", "1")
+    monkeypatch.setenv("SHIRO_HOT_MIN_MB", "0")
+    rng = np.random.default_rng(P * 5 + N)
+    n = 3000
+    row_ptr, col = hub_matrix(rng, n, 2500, 0.004)
+    val = rng.integers(1, 5, col.size).astype(np.float32)
+    B = rng.integers(0, 8, (n, N)).astype(np.float32)
+    ref = oracle.spmm_ref(row_ptr, col, val, B)
+    if P == 1:
+        pl = sh.Plan.distributed(0, 1, n, np.array([0, n], np.int64), row_ptr, col, val, N)
+        for k in (1, 2, 3):            # the copy is redone every step
+            Bd = torch.from_numpy(k * B).cuda()
+            Cd = torch.full((n, N), float("nan"), device="cuda")
+            pl.spmm(Bd, Cd)
+            torch.cuda.synchronize()
+            assert np.array_equal(Cd.cpu().numpy().astype(np.float64), k * ref)
+            assert pl.last_launches() == 2
+        return
+    else:
+        C, _ = run_loopback(n, oracle.uniform_partition(n, P), row_ptr, col, val, B)
+    assert np.array_equal(C.astype(np.float64), ref)
+
+
 @pytest.mark.parametrize("cfg,P", [("c1", 1), ("c1", 2), ("c2", 1), ("c2", 2), ("c2", 4),
                                    ("c2", 8)])
 def test_config_parity(cfg, P):
