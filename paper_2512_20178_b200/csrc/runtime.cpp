@@ -658,7 +658,9 @@ int64_t run_spmm(const DevSpmm &d, const float *X0, int64_t n0, const float *X1,
     if (X1 || n0 != d.hot_base) throw Error(SHIRO_E_INTERNAL, "hot buffer op with a second source");
     n += launch_pack(d.hot.n, d.hot.src, d.hot.dst, X0, d.hot_buf, a.N, s);
     a.X1 = d.hot_buf;
-    if (hotbuf_window()) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    SHIRO_CK(cudaStreamIsCapturing(s, &cap));
+    if (hotbuf_window() && cap == cudaStreamCaptureStatusNone) {   // direct launches only
       cudaStreamAttrValue v = {};
       v.accessPolicyWindow.base_ptr = d.hot_buf;
       v.accessPolicyWindow.num_bytes = (size_t)d.hot.n * a.N * sizeof(float);
